@@ -1,0 +1,168 @@
+"""Generate golden vectors from the REFERENCE implementation itself.
+
+Run in the build container only (it imports ``fasthog`` from the read-only
+reference checkout, which does not exist on the GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Writes ``tests/golden/lut_sha256.json`` and ``tests/golden/golden.npz``.
+Both are committed; tests pin the oracle (and through it the CUDA path)
+against them without needing the reference at run time.  Inputs are seeded
+so every case can be regenerated bit-for-bit from the recipe below.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+sys.path.insert(0, REF)
+
+import fasthog as fh  # noqa: E402  (the reference)
+
+from paper_1703_06256_b200 import synth  # noqa: E402
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def image_cases():
+    """(name, planes, bins) small seeded images covering gray/RGB/odd sizes."""
+    rng = np.random.default_rng(20260101)
+    cases = [
+        ("gray45x37", rng.integers(0, 256, (1, 37, 45), dtype=np.uint8), 9),
+        ("rgb48x40", rng.integers(0, 256, (3, 40, 48), dtype=np.uint8), 9),
+        ("gray133x77", rng.integers(0, 256, (1, 77, 133), dtype=np.uint8), 8),
+        ("rgb3x3", rng.integers(0, 256, (3, 3, 3), dtype=np.uint8), 4),
+        ("gray300x200_b18", rng.integers(0, 256, (1, 200, 300), dtype=np.uint8), 18),
+    ]
+    # identical channels (tie rule) and a blurred config-like frame
+    p = rng.integers(0, 256, (1, 50, 70), dtype=np.uint8)
+    cases.append(("rgbtie70x50", np.concatenate([p, p, p]), 9))
+    cfg = synth.CONFIGS["c2"]
+    cases.append(("c2frame0_crop", synth.make_frame(cfg, 0)[:, :160, :200].copy(), 8))
+    return cases
+
+
+def main():
+    out = {}
+    lut_hash = {}
+    for n in range(fh.gradient.MIN_BINS, fh.gradient.MAX_BINS + 1):
+        lut_hash[str(n)] = sha(fh.build_lut(n).table.astype("<i2"))
+    with open(os.path.join(HERE, "lut_sha256.json"), "w") as f:
+        json.dump(lut_hash, f, indent=1, sort_keys=True)
+    for n in (8, 9):
+        out[f"lut{n}"] = fh.build_lut(n).table.astype(np.int8)
+
+    geoms = {
+        "g16b2": fh.DescriptorGeometry(16, 16, 8, block=2, block_stride=1, bins=9),
+        "g16x24": fh.DescriptorGeometry(16, 24, 8, block=2, block_stride=1, bins=9),
+    }
+    for name, planes, bins in image_cases():
+        img = fh.Image(planes)
+        lut = fh.build_lut(bins)
+        bm = fh.gradient_map(img, lut)
+        st = fh.build_integral_stack(bm)
+        out[f"{name}/image"] = planes
+        out[f"{name}/bins"] = np.array(bins)
+        out[f"{name}/binmap"] = bm.cells
+        if st.planes.size <= 200_000:
+            out[f"{name}/planes"] = st.planes
+        out[f"{name}/planes_sha"] = np.array(sha(st.planes))
+        H, W = bm.height, bm.width
+        for gname, g0 in geoms.items():
+            if g0.bins != bins or g0.window_w > W or g0.window_h > H:
+                continue
+            for norm in ("none", "l1", "l2"):
+                g = fh.DescriptorGeometry(g0.window_w, g0.window_h, g0.cell, g0.block,
+                                          g0.block_stride, g0.bins, norm)
+                for stride in (1, 3, 8):
+                    key = f"{name}/{gname}/{norm}/s{stride}"
+                    oxs, oys = fh.window_origins(W, H, g, stride)
+                    cache = fh.CellHistogramCache(st, g, oxs, oys)
+                    descs = np.stack([d for _, _, d in fh.scan_descriptors(st, g, stride)])
+                    if norm == "none":
+                        out[f"{key}/grid"] = cache.grid
+                    if descs.size <= 60_000:
+                        out[f"{key}/descs"] = descs
+                    out[f"{key}/descs_sha"] = np.array(sha(descs))
+            # scores through scan() with seeded weights
+            g = g0
+            wrng = np.random.default_rng(77)
+            model = fh.LinearModel(g, wrng.normal(size=fh.descriptor_length(g)), 0.125)
+            for stride in (2, 4):
+                dets = fh.scan(st, model, stride, float("-inf"))
+                out[f"{name}/{gname}/scan_s{stride}/xy"] = np.array(
+                    [(d.x, d.y) for d in dets], dtype=np.int64)
+                out[f"{name}/{gname}/scan_s{stride}/score"] = np.array(
+                    [d.score for d in dets], dtype=np.float64)
+                out[f"{name}/{gname}/weights"] = model.weights
+        # block=1 BASELINE-style geometry on the larger images (cell 8, 16x32 window)
+        if W >= 64 and H >= 64:
+            for norm in ("none", "l2"):
+                g = fh.DescriptorGeometry(16, 32, 8, block=1, block_stride=1, bins=bins,
+                                          normalization=norm)
+                for stride in (4, 8):
+                    key = f"{name}/b1_{norm}/s{stride}"
+                    oxs, oys = fh.window_origins(W, H, g, stride)
+                    cache = fh.CellHistogramCache(st, g, oxs, oys)
+                    if norm == "none":
+                        out[f"{key}/grid"] = cache.grid
+                    wrng = np.random.default_rng(99)
+                    model = fh.LinearModel(g, wrng.normal(0, 0.01, fh.descriptor_length(g)), 0.0)
+                    dets = fh.scan(st, model, stride, float("-inf"))
+                    out[f"{key}/score"] = np.array([d.score for d in dets])
+                    out[f"{key}/weights"] = model.weights
+
+    # config c1 at full size: hashes of every stage and the score map
+    cfg = synth.CONFIGS["c1"]
+    frame = synth.make_frame(cfg, 0)
+    w, bias = synth.make_weights(cfg)
+    g = fh.DescriptorGeometry(64, 128, 8, block=1, block_stride=1, bins=cfg.bins)
+    bm = fh.gradient_map(fh.Image(frame), fh.build_lut(cfg.bins))
+    st = fh.build_integral_stack(bm)
+    oxs, oys = fh.window_origins(cfg.width, cfg.height, g, cfg.stride)
+    cache = fh.CellHistogramCache(st, g, oxs, oys)
+    dets = fh.scan(st, fh.LinearModel(g, w, bias), cfg.stride, float("-inf"))
+    out["c1/frame_sha"] = np.array(sha(frame))
+    out["c1/binmap_sha"] = np.array(sha(bm.cells))
+    out["c1/planes_sha"] = np.array(sha(st.planes))
+    out["c1/grid_sha"] = np.array(sha(cache.grid))
+    out["c1/scores"] = np.array([d.score for d in dets]).reshape(len(oys), len(oxs))
+
+    # bilinear resize (detector.py:202-221) and the pyramid level loop
+    rng = np.random.default_rng(4242)
+    src = rng.integers(0, 256, (3, 83, 97), dtype=np.uint8)
+    out["resize/src"] = src
+    for (nw, nh) in ((80, 69), (40, 33), (97, 83), (13, 7), (96, 82)):
+        out[f"resize/{nw}x{nh}"] = fh.detector._resize_bilinear(fh.Image(src), nw, nh).planes
+    big = synth.make_frame(synth.CONFIGS["c5"], 0)[:, :540, :960].copy()
+    out["resize_big/src_sha"] = np.array(sha(big))
+    for (nw, nh) in ((800, 450), (666, 375), (555, 312)):
+        out[f"resize_big/{nw}x{nh}_sha"] = np.array(
+            sha(fh.detector._resize_bilinear(fh.Image(big), nw, nh).planes))
+
+    g = fh.DescriptorGeometry(16, 16, 8, block=2, block_stride=1, bins=9)
+    pimg = np.random.default_rng(515).integers(0, 256, (1, 61, 83), dtype=np.uint8)
+    model = fh.LinearModel(g, np.random.default_rng(516).normal(size=36), -0.5)
+    dets = fh.pyramid_scan(fh.Image(pimg), model, 1.3, 4, float("-inf"))
+    out["pyramid/image"] = pimg
+    out["pyramid/weights"] = model.weights
+    out["pyramid/boxes"] = np.array([(d.x, d.y, d.w, d.h) for d in dets], dtype=np.int64)
+    out["pyramid/score"] = np.array([d.score for d in dets])
+    out["pyramid/scale"] = np.array([d.scale for d in dets])
+
+    np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
+    print(f"wrote {len(out)} arrays; npz size "
+          f"{os.path.getsize(os.path.join(HERE, 'golden.npz')) / 1e3:.0f} kB")
+
+
+if __name__ == "__main__":
+    main()
