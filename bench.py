@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the LUT-HOG hot path on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step is one pass of the hot path (LUT binning -> N_b int32 integral planes
+-> cell-histogram grid [-> per-cell L2 / window scores]) over one batch of a
+BASELINE configuration (default c2 = BASELINE.json configs[1]: 512 blurred
+640x480 frames, N_b=8, 64x128 windows at stride 4).  Frames are independent:
+under torchrun each rank runs its own batch of distinct frames (weak scaling,
+no collective on the data path); timings are max over ranks.
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port in oracle/, all host threads) on a bounded sample of the same
+workload; only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+NVML_REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=0, help="override frames per GPU (debug)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def workload_name(cfg) -> str:
+    kind = "i.i.d. uniform noise" if cfg.sigma is None else f"blurred noise sigma={cfg.sigma}"
+    extra = f" + {cfg.rects} rects" if cfg.rects else ""
+    tail = ", linear score" if cfg.scored else ""
+    norm = f", per-cell {cfg.normalization}" if cfg.normalization != "none" else ""
+    return (f"{cfg.key}: {cfg.frames}x {cfg.channels}x{cfg.height}x{cfg.width} u8 ({kind}{extra}), "
+            f"N_b={cfg.bins}, cell 8, 64x128 windows stride {cfg.stride}{norm}{tail}")
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(config_key):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(config_key, {}).get("k_planes_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML poller for SM clock + throttle reasons during the timed region."""
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self._h = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            import torch
+
+            h = None
+            try:
+                uuid = str(torch.cuda.get_device_properties(dev_index).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(("GPU-" + uuid).encode())
+            except Exception:
+                h = None
+            if h is None:
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+                idx = int(vis.split(",")[dev_index]) if vis and vis.split(",")[0].isdigit() else dev_index
+                h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self._nv, self._h = pynvml, h
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._h = None
+
+    def _poll(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(0.002)
+
+    def sample(self):
+        if self._h is None:
+            return
+        nv = self._nv
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+        except Exception:
+            pass
+
+    def start(self):
+        if self._h is None:
+            return
+        self._t = threading.Thread(target=self._poll, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        if self._h is None:
+            return None
+        self._stop.set()
+        self._t.join()
+        self.sample()
+        names = [n for b, n in NVML_REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+def gen_frames(cfg, first, count):
+    from paper_1703_06256_b200 import synth
+
+    return synth.make_batch(cfg, first, count)
+
+
+# --------------------------------------------------------------------------
+# CPU legs (oracle port): cpu_baseline and --impl reference
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_run(cfg, frames, threads):
+    from oracle import oracle as O
+    from paper_1703_06256_b200 import synth
+
+    lut = O.build_lut(cfg.bins)
+    mode = 1 if cfg.scored else (2 if cfg.normalization == "l2" else 0)
+    w, b = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
+    t0 = time.perf_counter()
+    O.run_batch(frames, lut, cfg.bins, 8, 64, 128, cfg.stride, mode, w, b, threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_sample_size(cfg, frames1, threads, seconds):
+    t1 = cpu_run(cfg, frames1[:1], 1)
+    return max(threads, min(cfg.frames, int(seconds * threads / max(t1, 1e-3)))), t1
+
+
+def cpu_baseline(cfg, seconds):
+    threads = host_threads()
+    probe = gen_frames(cfg, 0, 1)
+    count, t1 = cpu_sample_size(cfg, probe, threads, seconds)
+    frames = gen_frames(cfg, 0, count)
+    dt = cpu_run(cfg, frames, threads)
+    px = count * cfg.height * cfg.width
+    return {"value": px / dt / 1e6, "unit": "Mpixel/s", "cores": threads, "kind": "port",
+            "sample": f"{count} of {cfg.frames} {cfg.key} frames (oracle/hog_oracle.c, "
+                      f"{threads} threads, {dt:.1f} s; 1 frame on 1 thread: {t1 * 1e3:.0f} ms)",
+            "single_thread_mpx_s": cfg.height * cfg.width / t1 / 1e6}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = host_threads()
+    probe = gen_frames(cfg, 0, 1)
+    # each step: a bounded sample sized for ~3 s of all-core CPU work
+    per_step, t1 = cpu_sample_size(cfg, probe, threads, 3.0)
+    frames = gen_frames(cfg, 0, per_step)
+    for _ in range(args.warmup):
+        cpu_run(cfg, frames, threads)
+    times = [cpu_run(cfg, frames, threads) for _ in range(args.steps)]
+    ms = statistics.mean(times) * 1e3
+    px = per_step * cfg.height * cfg.width
+    value = px / (ms / 1e3) / 1e6
+    line = {
+        "impl": "reference", "metric": "Mpixel/s (LUT binning + per-bin integral planes + window HOG)",
+        "value": value, "unit": "Mpixel/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": workload_name(cfg), "frames_per_step": per_step,
+                   "implementation": "reference algorithm restated in C (oracle/, pinned to "
+                                     "the reference's golden vectors), all host threads"},
+        "cpu_baseline": {"value": value, "unit": "Mpixel/s", "cores": threads, "kind": "port",
+                         "sample": f"{per_step} of {cfg.frames} {cfg.key} frames per step"},
+        "e2e": {"value": value, "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+# GPU leg
+
+def main():
+    args = parse_args()
+    from paper_1703_06256_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1703_06256_b200 as H
+    from paper_1703_06256_b200.errors import PathMismatch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    nf = args.frames or cfg.frames
+    first = rank * nf  # each rank: its own shard of distinct frames
+    frames = gen_frames(cfg, first, nf)
+    weights, bias = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
+    p = H.HogPipeline(nf, cfg.channels, cfg.height, cfg.width, cfg.bins, stride=cfg.stride,
+                      normalization=cfg.normalization, weights=weights, bias=bias, device=dev)
+    p.upload(frames)
+    p.run()
+    torch.cuda.synchronize()
+
+    # parity gate before any timing (reference bench.py:147-166 pattern)
+    from oracle import oracle as O
+
+    check = [0, nf - 1] if nf > 1 else [0]
+    mode = 1 if cfg.scored else (2 if cfg.normalization == "l2" else 0)
+    _, g_ref, s_ref = O.run_batch(frames[check], O.build_lut(cfg.bins), cfg.bins, 8, 64, 128,
+                                  cfg.stride, mode, weights, bias, threads=2, want_outputs=True)
+    if not np.array_equal(p.grid[check].cpu().numpy().astype(np.int64), g_ref):
+        raise PathMismatch("GPU cell grid differs from the oracle; refusing to time")
+    if cfg.scored:
+        s = p.scores[check].cpu().numpy()
+        if (np.abs(s - s_ref) > 1e-5 * np.abs(s_ref) + 1e-12).any():
+            raise PathMismatch("GPU scores differ from the oracle beyond 1e-5; refusing to time")
+
+    K, W = args.steps, args.warmup
+    for _ in range(W):
+        p.run()
+    torch.cuda.synchronize()
+    stage = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    for evs in stage:  # materialise the CUDA events before handing them to the library
+        for e in evs:
+            e.record()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    start.record()
+    for i in range(K):
+        p.run(stage_events=stage[i])
+    end.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    barrier()
+    total_ms = start.elapsed_time(end)
+    plane_ms = sum(stage[i][2].elapsed_time(stage[i][3]) for i in range(K)) / K
+    bin_ms = sum(stage[i][0].elapsed_time(stage[i][1]) for i in range(K)) / K
+    scan_ms = sum(stage[i][1].elapsed_time(stage[i][2]) for i in range(K)) / K
+    total_ms, plane_ms, bin_ms, scan_ms = max_over_ranks([total_ms, plane_ms, bin_ms, scan_ms])
+    ms_per_step = total_ms / K
+    px_step = world * nf * cfg.height * cfg.width
+    value = px_step / (ms_per_step / 1e3) / 1e6
+
+    peak, peak_src = measured_peak()
+    plane_bytes = p.plane_kernel_bytes_per_frame() * nf
+    achieved = plane_bytes / (plane_ms / 1e3) / 1e9
+    traffic = ncu_traffic(cfg.key)
+    step_bytes = p.bytes_alg_per_frame() * nf
+    step_gbs = step_bytes / (ms_per_step / 1e3) / 1e9
+
+    # end to end through the public API: pinned host frames in, result out, per step
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": "Mpixel/s (LUT binning + per-bin integral planes + window HOG)",
+            "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32" if not cfg.scored else "int32+f64",
+            "data": "synthetic",
+            "config": {"workload": workload_name(cfg), "frames_per_gpu": nf,
+                       "global_frames": world * nf,
+                       "parallelism": f"frame-sharded x{world}, no collective",
+                       "l2": f"inputs larger than L2 ({step_bytes / 1e9:.2f} GB compulsory "
+                             f"traffic per GPU per step vs 126 MB L2)",
+                       "stages_ms": {"grad_bin": bin_ms, "carry_scans": scan_ms,
+                                     "planes_grid": plane_ms},
+                       "fused_grid": bool(p.fused)},
+            "roofline": {"bound": "hbm", "kernel": "k_planes", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_source": peak_src,
+                         "alg_bytes_per_launch": plane_bytes,
+                         "alg_bytes_def": "bin map read (1 B/px) + int32 planes written "
+                                          "(4*N_b*(H+1)*(W+1)) + int32 cell grid written"},
+            "pipeline_roofline": {"achieved": step_gbs, "peak": peak, "unit": "GB/s",
+                                  "frac": step_gbs / peak,
+                                  "alg_bytes_per_step": step_bytes,
+                                  "alg_bytes_def": "SURVEY 8d bytes_alg per frame x frames"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": p.launches_per_run() * K,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier):
+    """Per step: H2D of every frame from pinned host memory, the pipeline, and
+    D2H of the step's result, chunked over two streams so copies overlap
+    compute."""
+    import torch
+
+    from paper_1703_06256_b200 import synth
+
+    chunk = max(1, min(nf, 64))
+    nchunks = (nf + chunk - 1) // chunk
+    weights, bias = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
+    slots = []
+    for _ in range(min(2, nchunks)):
+        q = H.HogPipeline(chunk, cfg.channels, cfg.height, cfg.width, cfg.bins,
+                          stride=cfg.stride, normalization=cfg.normalization, weights=weights,
+                          bias=bias, device=dev)
+        slots.append((q, torch.cuda.Stream(device=dev)))
+    host_in = torch.from_numpy(frames).pin_memory()
+    res = slots[0][0].result()
+    host_out = torch.empty((nf,) + tuple(res.shape[1:]), dtype=res.dtype).pin_memory()
+    cur = torch.cuda.current_stream()
+
+    def step():
+        for s in (st for _, st in slots):
+            s.wait_stream(cur)
+        for j in range(nchunks):
+            q, st = slots[j % len(slots)]
+            a, b = j * chunk, min(nf, (j + 1) * chunk)
+            with torch.cuda.stream(st):
+                dst = q.frames.data if q.frames.pitch == cfg.width else q.frames.data[..., : cfg.width]
+                dst[: b - a].copy_(host_in[a:b], non_blocking=True)
+                q.run(stream=st)
+                host_out[a:b].copy_(q.result()[: b - a], non_blocking=True)
+        for _, st in slots:
+            cur.wait_stream(st)
+
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(K):
+        step()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks([t0.elapsed_time(t1) / K])[0]
+    # the D2H result must equal the device-resident run's result
+    ok = bool(torch.equal(host_out.to(dev), p.result().to(host_out.dtype)))
+    return {"value": world * nf * cfg.height * cfg.width / (ms / 1e3) / 1e6, "unit": "Mpixel/s",
+            "ms_per_step": ms, "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
+            "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
+            "result": "cell grid" if not cfg.scored else "window scores",
+            "chunk_frames": chunk, "streams": len(slots), "matches_device_run": ok}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,135 @@
+/*
+ * hogb200.h -- C ABI of libhogb200.so, the sm_100a LUT-HOG hot path.
+ *
+ * The reference (fasthog, pure Python + NumPy) has no FFI; its drop-in
+ * surface is the flat Python API in pkg/src/fasthog/__init__.py:4-65.
+ * Each entry point below replaces the NumPy body of one reference function
+ * (paths relative to /root/reference/pkg/src/fasthog/), and the Python
+ * package paper_1703_06256_b200 binds them with ctypes under the reference's
+ * own function names.
+ *
+ * Conventions
+ *   - Every buffer pointer is a DEVICE pointer owned by the caller (torch
+ *     tensors in the Python layer).  The library allocates nothing.
+ *   - Strides are in elements of the pointed-to type (bytes for uint8/int8).
+ *   - All calls are asynchronous on `stream` (NULL = legacy default stream),
+ *     reentrant, and never synchronise the host.
+ *   - Return 0 on success, HOG_EINVAL for a rejected argument, HOG_ECUDA for
+ *     a launch error; hog_last_error() describes the last failure (per thread).
+ *
+ * Data layouts
+ *   image   uint8  [n][c][h][w]   elem (f,ch,y,x) = img[f*img_fstride + ch*img_cstride + y*img_pitch + x]
+ *                                 img_pitch % 4 == 0, img_pitch >= round_up(w, 4), 4-byte aligned base
+ *   binmap  int8   [n][h][w]      elem (f,y,x) = bm[f*bm_fstride + y*bm_pitch + x], -1 = NO_BIN
+ *                                 bm_pitch % 4 == 0, bm_pitch >= round_up(w, 4)
+ *   planes  int32  [n][bins][h+1][w+1]
+ *                                 elem (f,b,Y,X) = pl[f*pl_fstride + b*pl_nstride + Y*pl_pitch + X]
+ *                                 pl_pitch >= w+1.  Fast path (16-B vector stores) when
+ *                                 (pl + 1) is 16-B aligned and pl_pitch, pl_nstride, pl_fstride
+ *                                 are multiples of 4 and pl_pitch >= w + 4; otherwise scalar stores.
+ *                                 hog_plane_pitch(w) returns the fast-path pitch.
+ *   grid    int32  [n][ncy][ncx][bins]  cell histograms (CellHistogramCache.grid, descriptor.py:176-185)
+ */
+#ifndef HOGB200_H
+#define HOGB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *hog_stream_t; /* == cudaStream_t */
+
+#define HOG_OK 0
+#define HOG_EINVAL 1
+#define HOG_ECUDA 2
+
+/* Library version string, e.g. "hogb200 1.0 sm_100a". */
+const char *hog_version(void);
+
+/* Text of the last error raised on the calling thread ("" if none). */
+const char *hog_last_error(void);
+
+/* Fast-path plane row pitch (elements) for width w: round_up(w + 4, 8). */
+int64_t hog_plane_pitch(int w);
+
+/* gradient.py:95-121 (gradient_map) + gradient.py:56-72 (the table itself
+ * is host-built, as in the reference, and uploaded as uint8 with -1 -> 0xFF;
+ * lut is 511*511 bytes indexed (dx+255)*511 + (dy+255)).  c in {1, 3}.
+ * Writes the bin map; border and zero-gradient pixels get -1. */
+int hog_grad_bin(const uint8_t *img, int n, int c, int h, int w,
+                 int64_t img_pitch, int64_t img_cstride, int64_t img_fstride,
+                 const uint8_t *lut, int bins,
+                 int8_t *binmap, int64_t bm_pitch, int64_t bm_fstride,
+                 hog_stream_t stream);
+
+/* Scratch needed by hog_integral / hog_pipeline for this shape. */
+size_t hog_scratch_bytes(int n, int h, int w, int bins, int stride, int cell);
+
+/* integral.py:58-87 (build_integral_stack, 32-bit accumulators): the N_b
+ * padded summed-area tables of a bin map, every plane element written once. */
+int hog_integral(const int8_t *binmap, int n, int h, int w, int64_t bm_pitch, int64_t bm_fstride,
+                 int bins, int32_t *planes, int64_t pl_pitch, int64_t pl_nstride,
+                 int64_t pl_fstride, void *scratch, size_t scratch_bytes, hog_stream_t stream);
+
+/* Fused LUT-HOG pipeline over a frame batch: gradient + LUT binning
+ * (gradient.py:95-121) -> integral planes (integral.py:58-87) -> cell
+ * histogram grid by 4-corner reads (descriptor.py:162-188), for the regular
+ * cell lattice produced by a stride-s scan (cell origins = multiples of
+ * `stride` up to ((ncx-1)*stride, (ncy-1)*stride)).  grid may be NULL (no
+ * cell grid).  Requires stride % 4 == 0, cell % stride == 0, cell/stride <= 2
+ * when grid != NULL; otherwise use hog_integral + hog_cell_grid.
+ * stage_events: NULL, or 4 cudaEvent_t recorded on `stream` before the
+ * binning kernel, before the carry scans, before the plane kernel and after
+ * it (lets a caller time each stage inside a larger timed region). */
+int hog_pipeline(const uint8_t *img, int n, int c, int h, int w,
+                 int64_t img_pitch, int64_t img_cstride, int64_t img_fstride,
+                 const uint8_t *lut, int bins,
+                 int8_t *binmap, int64_t bm_pitch, int64_t bm_fstride,
+                 int32_t *planes, int64_t pl_pitch, int64_t pl_nstride, int64_t pl_fstride,
+                 int cell, int stride, int ncx, int ncy, int32_t *grid,
+                 void *scratch, size_t scratch_bytes, void *const *stage_events,
+                 hog_stream_t stream);
+
+/* descriptor.py:176-185 for an arbitrary (sorted) cell-origin set:
+ * grid[f][j][i][b] = 4-corner count of the cell at (cell_ys[j], cell_xs[i]). */
+int hog_cell_grid(const int32_t *planes, int n, int h, int w, int bins,
+                  int64_t pl_pitch, int64_t pl_nstride, int64_t pl_fstride,
+                  const int32_t *cell_xs, int ncx, const int32_t *cell_ys, int ncy, int cell,
+                  int32_t *grid, hog_stream_t stream);
+
+/* descriptor.py:94-104/119-124 for block == 1: one denominator per cell,
+ * norm 1 (l1): sum|v| + eps_term, norm 2 (l2): sqrt(sum v^2 + eps_term).
+ * denom is [n][ncells] float64.  Pass eps_term = _EPS (l1) or _EPS*_EPS (l2). */
+int hog_cell_norm(const int32_t *grid, int n, int ncells, int bins, int norm, double eps_term,
+                  double *denom, hog_stream_t stream);
+
+/* descriptor.py:107-124 (_assemble_blocks) + detector.py:140-154 (scores):
+ * for every window (iy, ix) of the scan, the descriptor is assembled from
+ * grid[row_idx[iy][*]][col_idx[ix][*]] (descriptor.py:190-195) with the
+ * block geometry and per-block normalisation (0 none, 1 l1, 2 l2), and
+ *   scores[f][iy][ix] = dot(weights, descriptor) + bias      (if scores)
+ *   desc[f][iy][ix][:] = descriptor (float64)                  (if desc)
+ * row_idx is [noy][cells_y], col_idx is [nox][cells_x] (int32). */
+int hog_window_features(const int32_t *grid, int n, int ncy, int ncx, int bins,
+                        const int32_t *row_idx, int noy, const int32_t *col_idx, int nox,
+                        int cells_x, int cells_y, int block, int block_stride,
+                        int norm, double eps_term, const double *weights, double bias,
+                        double *scores, double *desc, hog_stream_t stream);
+
+/* detector.py:202-221 (_resize_bilinear): separable bilinear, pixel centres
+ * aligned, float64 in the reference's operation order (no FMA contraction),
+ * rint half-even, clip to 0..255.  ry = h / nh and rx = w / nw as computed by
+ * the caller in float64. */
+int hog_resize_bilinear(const uint8_t *src, int n, int c, int h, int w,
+                        int64_t src_pitch, int64_t src_cstride, int64_t src_fstride,
+                        int nh, int nw, double ry, double rx,
+                        uint8_t *dst, int64_t dst_pitch, int64_t dst_cstride, int64_t dst_fstride,
+                        hog_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOGB200_H */

@@ -1,0 +1,181 @@
+"""Device buffers for the LUT-HOG path (torch tensors used as plain HBM
+allocations; the compute is libhogb200.so).
+
+HBM layouts (include/hogb200.h):
+  frames  uint8 (N, C, H, Wp)        Wp = round_up(W, 4)   (pitched rows)
+  binmap  int8  (N, H, Wp)           -1 = NO_BIN
+  planes  int32 (N, bins, H+1, Pp)   Pp = round_up(W + 4, 8); the tensor view
+                                     starts 7 elements into its allocation so
+                                     plane column 1 of every row is 32-byte
+                                     aligned and each lane's 16-B store is one
+                                     aligned half-sector.
+  grid    int32 (N, ncy, ncx, bins)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+
+
+def torch():
+    import torch as _t
+
+    return _t
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise _native.NativeUnavailable(
+            "no CUDA device: the LUT-HOG path runs only on the GPU (no CPU fallback)")
+    _native.load()
+    return t
+
+
+def round_up(v: int, m: int) -> int:
+    return (v + m - 1) // m * m
+
+
+def stream_handle(stream=None) -> int:
+    t = torch()
+    s = stream if stream is not None else t.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(x) -> int:
+    return int(x.data_ptr())
+
+
+@dataclass
+class DevFrames:
+    """Pitched uint8 frames (N, C, H, pitch) on the device."""
+
+    data: object
+    n: int
+    c: int
+    h: int
+    w: int
+
+    @property
+    def pitch(self) -> int:
+        return self.data.shape[-1]
+
+    @property
+    def cstride(self) -> int:
+        return self.h * self.pitch
+
+    @property
+    def fstride(self) -> int:
+        return self.c * self.h * self.pitch
+
+
+def alloc_frames(n, c, h, w, device=None) -> DevFrames:
+    t = require_cuda()
+    data = t.empty((n, c, h, round_up(w, 4)), dtype=t.uint8, device=device or "cuda")
+    return DevFrames(data, n, c, h, w)
+
+
+def upload_frames(frames: np.ndarray, device=None, out: DevFrames | None = None) -> DevFrames:
+    """(N,C,H,W) or (C,H,W) uint8 host array -> pitched device frames."""
+    t = require_cuda()
+    a = np.asarray(frames, dtype=np.uint8)
+    if a.ndim == 3:
+        a = a[None]
+    n, c, h, w = a.shape
+    df = out or alloc_frames(n, c, h, w, device)
+    if df.pitch == w:
+        df.data.copy_(t.from_numpy(np.ascontiguousarray(a)), non_blocking=False)
+    else:
+        df.data[..., :w].copy_(t.from_numpy(np.ascontiguousarray(a)))
+    return df
+
+
+@dataclass
+class DevBinmap:
+    data: object  # int8 (N, H, pitch)
+    n: int
+    h: int
+    w: int
+
+    @property
+    def pitch(self) -> int:
+        return self.data.shape[-1]
+
+    @property
+    def fstride(self) -> int:
+        return self.h * self.pitch
+
+    def view(self):
+        return self.data[..., : self.w]
+
+
+def alloc_binmap(n, h, w, device=None) -> DevBinmap:
+    t = require_cuda()
+    return DevBinmap(t.empty((n, h, round_up(w, 4)), dtype=t.int8, device=device or "cuda"),
+                     n, h, w)
+
+
+@dataclass
+class DevPlanes:
+    base: object  # int32 allocation
+    n: int
+    bins: int
+    h: int
+    w: int
+    pitch: int
+    offset: int = 7
+
+    @property
+    def nstride(self) -> int:
+        return (self.h + 1) * self.pitch
+
+    @property
+    def fstride(self) -> int:
+        return self.bins * self.nstride
+
+    @property
+    def ptr(self) -> int:
+        return ptr(self.base) + 4 * self.offset
+
+    def view(self):
+        """(N, bins, H+1, W+1) int32 strided view of the logical planes."""
+        flat = self.base[self.offset: self.offset + self.n * self.fstride]
+        return flat.view(self.n, self.bins, self.h + 1, self.pitch)[..., : self.w + 1]
+
+
+def alloc_planes(n, bins, h, w, device=None) -> DevPlanes:
+    t = require_cuda()
+    pitch = int(_native.load().hog_plane_pitch(w))
+    total = n * bins * (h + 1) * pitch + 8
+    base = t.empty(total, dtype=t.int32, device=device or "cuda")
+    return DevPlanes(base, n, bins, h, w, pitch)
+
+
+def scratch(n, h, w, bins, stride=0, cell=0, device=None):
+    t = require_cuda()
+    nbytes = int(_native.load().hog_scratch_bytes(n, h, w, bins, stride, cell))
+    return t.empty(max(nbytes, 256), dtype=t.uint8, device=device or "cuda"), nbytes
+
+
+_LUT_CACHE: dict = {}
+
+
+def lut_device(table: np.ndarray, device=None):
+    """Upload a (511,511) int16 table as uint8 (NO_BIN -1 -> 0xFF), cached by content."""
+    t = require_cuda()
+    tab = np.asarray(table)
+    dev = t.device(device or "cuda")
+    if dev.index is None:
+        dev = t.device("cuda", t.cuda.current_device())
+    key = (dev.index, tab.shape, tab.tobytes()[:64], hash(tab.tobytes()))
+    hit = _LUT_CACHE.get(key)
+    if hit is None:
+        if tab.shape != (511, 511):
+            raise ValueError("orientation table must be 511x511")
+        b = np.ascontiguousarray(tab.astype(np.int16)).astype(np.int8).view(np.uint8)
+        hit = t.from_numpy(b.copy()).to(dev)
+        _LUT_CACHE[key] = hit
+    return hit

@@ -1,0 +1,156 @@
+"""Batched device pipeline: the path the benchmark configurations run.
+
+One ``HogPipeline`` owns every HBM buffer for a frame batch of one shape and
+runs LUT binning -> integral planes -> cell grid (fused into the plane
+kernel when the scan lattice is regular) -> optional per-cell normalisation
+and window scores, entirely on one CUDA stream with no host synchronisation.
+Frames are independent, so multi-GPU runs give each rank its own pipeline
+over its own frame shard (no collective).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native, device as D
+from .descriptor import (DescriptorGeometry, cell_lattice, descriptor_length, eps_term,
+                         window_features_device, window_origins, _NORM_CODE)
+from .gradient import build_lut
+
+
+def regular_lattice(cell_xs, cell_ys, stride: int, cell: int, bins: int) -> bool:
+    """True when hog_pipeline can emit the grid from the plane kernel."""
+    if stride % 4 or cell % stride or cell // stride > 2 or cell % 4 or bins > 18:
+        return False
+    for cs in (cell_xs, cell_ys):
+        if len(cs) == 0 or not np.array_equal(cs, np.arange(0, cs[-1] + 1, stride)):
+            return False
+    return True
+
+
+class HogPipeline:
+    def __init__(self, n: int, channels: int, height: int, width: int, bins: int, *,
+                 stride: int, cell: int = 8, window=(64, 128), normalization: str = "none",
+                 weights=None, bias: float = 0.0, lut=None, device=None):
+        t = D.require_cuda()
+        self.n, self.c, self.h, self.w, self.bins = n, channels, height, width, bins
+        self.stride, self.cell = stride, cell
+        self.geometry = DescriptorGeometry(window[0], window[1], cell, block=1, block_stride=1,
+                                           bins=bins, normalization=normalization)
+        g = self.geometry
+        self.oxs, self.oys = window_origins(width, height, g, stride)
+        self.cell_xs, self.cell_ys, self.col_idx, self.row_idx = cell_lattice(self.oxs, self.oys, g)
+        self.ncx, self.ncy = len(self.cell_xs), len(self.cell_ys)
+        self.fused = regular_lattice(self.cell_xs, self.cell_ys, stride, cell, bins)
+        self.lut = lut or build_lut(bins)
+        self.device = t.device(device or "cuda")
+        dev = self.device
+        self.frames = D.alloc_frames(n, channels, height, width, dev)
+        self.binmap = D.alloc_binmap(n, height, width, dev)
+        self.planes = D.alloc_planes(n, bins, height, width, dev)
+        self.grid = t.empty((n, self.ncy, self.ncx, bins), dtype=t.int32, device=dev)
+        self.lut_dev = D.lut_device(self.lut.table, dev)
+        sb = int(_native.load().hog_scratch_bytes(n, height, width, bins,
+                                                  stride if self.fused else 0,
+                                                  cell if self.fused else 0))
+        self.scratch = t.empty(max(sb, 256), dtype=t.uint8, device=dev)
+        self.scratch_bytes = sb
+        self.cx_dev = t.as_tensor(self.cell_xs.astype(np.int32), device=dev)
+        self.cy_dev = t.as_tensor(self.cell_ys.astype(np.int32), device=dev)
+        self.denom = None
+        if normalization != "none":
+            self.denom = t.empty((n, self.ncy, self.ncx), dtype=t.float64, device=dev)
+        self.weights = None if weights is None else np.asarray(weights, dtype=np.float64)
+        self.bias = float(bias)
+        self.scores = None
+        if self.weights is not None:
+            if len(self.weights) != descriptor_length(g):
+                raise ValueError("weights length does not match the geometry")
+            self.scores = t.empty((n, len(self.oys), len(self.oxs)), dtype=t.float64, device=dev)
+            self.w_dev = t.as_tensor(self.weights, device=dev)
+            self.ri_dev = t.as_tensor(self.row_idx.astype(np.int32), device=dev)
+            self.ci_dev = t.as_tensor(self.col_idx.astype(np.int32), device=dev)
+
+    # -- data movement ------------------------------------------------------
+    def upload(self, frames: np.ndarray, stream=None):
+        t = D.torch()
+        src = t.from_numpy(np.ascontiguousarray(frames))
+        if self.frames.pitch == self.w:
+            self.frames.data.copy_(src, non_blocking=True)
+        else:
+            self.frames.data[..., : self.w].copy_(src, non_blocking=True)
+
+    # -- the hot path -------------------------------------------------------
+    def run(self, stream=None, stage_events=None):
+        """Enqueue the whole batch on `stream` (default: current).  stage_events:
+        optional 4 recorded torch.cuda.Events bracketing binning / scans / planes."""
+        s = D.stream_handle(stream)
+        evs = None
+        if stage_events is not None:
+            import ctypes
+            evs = (ctypes.c_void_p * 4)(*[e.cuda_event for e in stage_events])
+        fr, bm, pl = self.frames, self.binmap, self.planes
+        _native.call("hog_pipeline", D.ptr(fr.data), self.n, self.c, self.h, self.w,
+                     fr.pitch, fr.cstride, fr.fstride, D.ptr(self.lut_dev), self.bins,
+                     D.ptr(bm.data), bm.pitch, bm.fstride, pl.ptr, pl.pitch, pl.nstride,
+                     pl.fstride, self.cell, self.stride, self.ncx, self.ncy,
+                     D.ptr(self.grid) if self.fused else None, D.ptr(self.scratch),
+                     self.scratch_bytes, evs, s)
+        if not self.fused:
+            _native.call("hog_cell_grid", pl.ptr, self.n, self.h, self.w, self.bins, pl.pitch,
+                         pl.nstride, pl.fstride, D.ptr(self.cx_dev), self.ncx,
+                         D.ptr(self.cy_dev), self.ncy, self.cell, D.ptr(self.grid), s)
+        g = self.geometry
+        if self.denom is not None:
+            _native.call("hog_cell_norm", D.ptr(self.grid), self.n, self.ncx * self.ncy,
+                         self.bins, _NORM_CODE[g.normalization], eps_term(g.normalization),
+                         D.ptr(self.denom), s)
+        if self.scores is not None:
+            _native.call("hog_window_features", D.ptr(self.grid), self.n, self.ncy, self.ncx,
+                         self.bins, D.ptr(self.ri_dev), len(self.oys), D.ptr(self.ci_dev),
+                         len(self.oxs), g.cells_x, g.cells_y, 1, 1, _NORM_CODE[g.normalization],
+                         eps_term(g.normalization), D.ptr(self.w_dev), self.bias,
+                         D.ptr(self.scores), None, s)
+
+    def launches_per_run(self) -> int:
+        k = 5  # grad_bin + 3 scans + planes
+        k += 0 if self.fused else 1
+        k += 1 if self.denom is not None else 0
+        k += 1 if self.scores is not None else 0
+        return k
+
+    # -- views ----------------------------------------------------------------
+    def planes_view(self):
+        return self.planes.view()
+
+    def binmap_view(self):
+        return self.binmap.view()
+
+    def result(self):
+        """The step's result tensor (what a caller reads back)."""
+        if self.scores is not None:
+            return self.scores
+        if self.denom is not None:
+            return self.denom
+        return self.grid
+
+    def normalized_grid(self):
+        """Per-cell normalised histograms (descriptor.py:119-124 with block=1)."""
+        return self.grid.to(D.torch().float64) / self.denom[..., None]
+
+    def bytes_alg_per_frame(self) -> int:
+        """SURVEY §8d compulsory bytes per frame."""
+        H, W, C, nb = self.h, self.w, self.c, self.bins
+        b = C * H * W + H * W + 4 * nb * (H + 1) * (W + 1) + 4 * nb * self.ncx * self.ncy
+        if self.scores is not None:
+            b += 8 * len(self.oxs) * len(self.oys)
+        if self.denom is not None:
+            b += 8 * self.ncx * self.ncy
+        return b
+
+    def plane_kernel_bytes_per_frame(self) -> int:
+        """Algorithmic bytes of k_planes per frame: bin map read + planes + grid written."""
+        H, W, nb = self.h, self.w, self.bins
+        b = H * W + 4 * nb * (H + 1) * (W + 1)
+        if self.fused:
+            b += 4 * nb * self.ncx * self.ncy
+        return b

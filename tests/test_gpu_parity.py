@@ -1,0 +1,261 @@
+"""Parity of the CUDA path (through the C ABI) with the reference's golden
+vectors and with the pinned CPU oracle.  Bit-exact for bin maps, planes,
+cell grids and normalised descriptors; scores within a stated tolerance.
+
+Score tolerance: |gpu - ref| <= 1e-12 * sum|w| * 64 + 1e-12 (absolute), far
+inside the north-star's 1e-5 relative bound; fp64 accumulation in a
+different order than OpenBLAS's ddot is the only source of difference.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1703_06256_b200 as H  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from paper_1703_06256_b200 import synth  # noqa: E402
+
+CASES = ["gray45x37", "rgb48x40", "gray133x77", "rgb3x3", "gray300x200_b18",
+         "rgbtie70x50", "c2frame0_crop"]
+
+
+def score_tol(w):
+    return 1e-12 * float(np.abs(w).sum()) * 64 + 1e-12
+
+
+def geom(gname, bins, norm="none"):
+    if gname == "g16b2":
+        return H.DescriptorGeometry(16, 16, 8, 2, 1, bins, norm)
+    return H.DescriptorGeometry(16, 24, 8, 2, 1, bins, norm)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_binmap_and_planes_golden(golden, name):
+    img, bins = golden[f"{name}/image"], int(golden[f"{name}/bins"])
+    bm = H.gradient_map(H.Image(img), H.build_lut(bins))
+    assert bm.cells.dtype == np.int16
+    assert np.array_equal(bm.cells, golden[f"{name}/binmap"])
+    st = H.build_integral_stack(bm)
+    assert st.planes.dtype == np.uint32
+    assert O.sha256(st.planes) == str(golden[f"{name}/planes_sha"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_grids_and_descriptors_golden(golden, name):
+    img, bins = golden[f"{name}/image"], int(golden[f"{name}/bins"])
+    st = H.build_integral_stack(H.gradient_map(H.Image(img), H.build_lut(bins)))
+    for gname in ("g16b2", "g16x24"):
+        for norm in ("none", "l1", "l2"):
+            for stride in (1, 3, 8):
+                key = f"{name}/{gname}/{norm}/s{stride}"
+                if f"{key}/descs_sha" not in golden.files:
+                    continue
+                g = geom(gname, bins, norm)
+                oxs, oys = H.window_origins(st.width, st.height, g, stride)
+                if norm == "none":
+                    cache = H.CellHistogramCache(st, g, oxs, oys)
+                    assert np.array_equal(cache.grid, golden[f"{key}/grid"])
+                descs = np.stack([d for _, _, d in H.scan_descriptors(st, g, stride)])
+                assert descs.dtype == (np.int64 if norm == "none" else np.float64)
+                assert O.sha256(descs) == str(golden[f"{key}/descs_sha"]), key
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_scan_scores_golden(golden, name):
+    img, bins = golden[f"{name}/image"], int(golden[f"{name}/bins"])
+    st = H.build_integral_stack(H.gradient_map(H.Image(img), H.build_lut(bins)))
+    for gname in ("g16b2", "g16x24"):
+        if f"{name}/{gname}/weights" not in golden.files:
+            continue
+        w = golden[f"{name}/{gname}/weights"]
+        model = H.LinearModel(geom(gname, bins), w, 0.125)
+        for stride in (2, 4):
+            dets = H.scan(st, model, stride, float("-inf"))
+            xy = np.array([(d.x, d.y) for d in dets])
+            assert np.array_equal(xy, golden[f"{name}/{gname}/scan_s{stride}/xy"])
+            np.testing.assert_allclose([d.score for d in dets],
+                                       golden[f"{name}/{gname}/scan_s{stride}/score"],
+                                       rtol=0, atol=score_tol(w))
+    for norm in ("none", "l2"):
+        for stride in (4, 8):
+            key = f"{name}/b1_{norm}/s{stride}"
+            if f"{key}/score" not in golden.files:
+                continue
+            g = H.DescriptorGeometry(16, 32, 8, 1, 1, bins, norm)
+            w = golden[f"{key}/weights"]
+            dets = H.scan(st, H.LinearModel(g, w, 0.0), stride, float("-inf"))
+            np.testing.assert_allclose([d.score for d in dets], golden[f"{key}/score"],
+                                       rtol=0, atol=score_tol(w))
+
+
+def test_config1_full_pipeline_golden(golden):
+    cfg = synth.CONFIGS["c1"]
+    frame = synth.make_frame(cfg, 0)
+    w, bias = synth.make_weights(cfg)
+    p = H.HogPipeline(1, 1, cfg.height, cfg.width, cfg.bins, stride=cfg.stride, weights=w,
+                      bias=bias)
+    assert p.fused
+    p.upload(frame[None])
+    p.run()
+    torch.cuda.synchronize()
+    assert O.sha256(p.binmap_view()[0].cpu().numpy().astype(np.int16)) == str(golden["c1/binmap_sha"])
+    planes = p.planes_view()[0].cpu().numpy().view(np.uint32)
+    assert O.sha256(planes) == str(golden["c1/planes_sha"])
+    grid = p.grid[0].cpu().numpy().astype(np.int64)
+    assert O.sha256(grid) == str(golden["c1/grid_sha"])
+    ref = golden["c1/scores"]
+    s = p.scores[0].cpu().numpy()
+    assert s.shape == ref.shape
+    assert (np.abs(s - ref) / np.abs(ref)).max() < 1e-10  # north star: 1e-5
+
+
+@pytest.mark.parametrize("key,count", [("c2", 3), ("c3", 2), ("c4", 2)])
+def test_config_batches_vs_oracle(key, count):
+    cfg = synth.CONFIGS[key]
+    frames = synth.make_batch(cfg, 0, count)
+    weights, bias = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
+    p = H.HogPipeline(count, cfg.channels, cfg.height, cfg.width, cfg.bins, stride=cfg.stride,
+                      normalization=cfg.normalization, weights=weights, bias=bias)
+    assert p.fused
+    p.upload(frames)
+    p.run()
+    torch.cuda.synchronize()
+    lut = O.build_lut(cfg.bins)
+    mode = 1 if cfg.scored else (2 if cfg.normalization == "l2" else 0)
+    _, grid, scores = O.run_batch(frames, lut, cfg.bins, 8, 64, 128, cfg.stride, mode,
+                                  weights, bias, threads=4, want_outputs=True)
+    assert np.array_equal(p.grid.cpu().numpy().astype(np.int64), grid)
+    # planes and bin map of the first frame, bit-exact
+    cells = O.gradient_map(frames[0], lut)
+    assert np.array_equal(p.binmap_view()[0].cpu().numpy().astype(np.int16), cells)
+    assert np.array_equal(p.planes_view()[0].cpu().numpy().view(np.uint32),
+                          O.integral_stack(cells, cfg.bins))
+    if cfg.scored:
+        np.testing.assert_allclose(p.scores.cpu().numpy(), scores, rtol=1e-5,
+                                   atol=score_tol(weights))
+        rel = np.abs(p.scores.cpu().numpy() - scores) / np.maximum(np.abs(scores), 1e-300)
+        assert np.median(rel) < 1e-12
+    if cfg.normalization == "l2":
+        g = grid.astype(np.float64)
+        den = np.sqrt((g * g).sum(axis=-1) + 1e-6 * 1e-6)
+        assert np.array_equal(p.denom.cpu().numpy(), den)
+        assert np.array_equal(p.normalized_grid().cpu().numpy(), g / den[..., None])
+
+
+def test_fused_grid_equals_generic_corner_reads():
+    # the fused-grid kernel and the generic 4-corner kernel on the same planes
+    cfg = synth.CONFIGS["c2"]
+    frames = synth.make_batch(cfg, 5, 4)
+    p = H.HogPipeline(4, 1, cfg.height, cfg.width, cfg.bins, stride=cfg.stride)
+    p.upload(frames)
+    p.run()
+    from paper_1703_06256_b200.descriptor import cell_grid_device
+
+    generic = cell_grid_device(p.planes, p.cell_xs, p.cell_ys, 8)
+    assert torch.equal(generic, p.grid)
+
+
+@pytest.mark.parametrize("w,h,c,bins", [(3, 3, 1, 8), (5, 4, 3, 9), (37, 29, 1, 8),
+                                        (129, 65, 1, 18), (255, 7, 3, 4), (641, 13, 1, 2),
+                                        (70, 66, 1, 30), (33, 31, 3, 64)])
+def test_odd_shapes_and_bin_counts_vs_oracle(w, h, c, bins):
+    rng = np.random.default_rng(w * 1000 + h * 10 + bins)
+    img = rng.integers(0, 256, (c, h, w), dtype=np.uint8)
+    lut = H.build_lut(bins)
+    bm = H.gradient_map(H.Image(img), lut)
+    ref = O.gradient_map(img, O.build_lut(bins))
+    assert np.array_equal(bm.cells, ref)
+    st = H.build_integral_stack(bm)
+    assert np.array_equal(st.planes, O.integral_stack(ref, bins))
+
+
+def test_user_binmap_with_out_of_range_values():
+    # integral.py:76: only cells == n count; other values (incl. -1) count nowhere
+    rng = np.random.default_rng(9)
+    cells = rng.integers(-3, 12, size=(40, 53)).astype(np.int16)
+    st = H.build_integral_stack(H.BinMap(9, cells))
+    ref = np.zeros((9, 41, 54), np.uint32)
+    for n in range(9):
+        ref[n, 1:, 1:] = np.cumsum(np.cumsum(cells == n, axis=0), axis=1)
+    assert np.array_equal(st.planes, ref)
+
+
+def test_acc_width_16():
+    cells = np.full((255, 255), -1, np.int16)
+    cells[1:-1, 1:-1] = 1
+    st = H.build_integral_stack(H.BinMap(4, cells), acc_width=16)
+    assert st.planes.dtype == np.uint16 and st.planes[1, 255, 255] == 253 * 253
+    with pytest.raises(H.AccumulatorOverflowRisk):
+        big = np.full((300, 300), 1, np.int16)
+        H.build_integral_stack(H.BinMap(4, big), acc_width=16)
+
+
+def test_constant_image_all_sentinel_and_zero_planes():
+    img = np.full((1, 17, 23), 128, np.uint8)
+    bm = H.gradient_map(H.Image(img), H.build_lut(8))
+    assert (bm.cells == H.NO_BIN).all()
+    assert not H.build_integral_stack(bm).planes.any()
+
+
+def test_errors_match_reference():
+    with pytest.raises(H.ImageTooSmall):
+        H.gradient_map(H.Image(np.zeros((1, 2, 5), np.uint8)), H.build_lut(8))
+    st = H.build_integral_stack(H.gradient_map(H.Image(np.zeros((1, 20, 20), np.uint8) + 5),
+                                               H.build_lut(8)))
+    g = H.DescriptorGeometry(16, 16, 8, 2, 1, 8)
+    with pytest.raises(H.WindowOutOfBounds):
+        H.window_descriptor(st, (5, 5), g)
+    with pytest.raises(H.InvalidGeometry):
+        H.window_descriptor(st, (0, 0), H.DescriptorGeometry(16, 16, 8, 2, 1, 9))
+    small = H.build_integral_stack(H.gradient_map(H.Image(np.zeros((1, 12, 12), np.uint8)),
+                                                  H.build_lut(9)))
+    with pytest.raises(H.WindowLargerThanImage):
+        H.scan(small, H.LinearModel(H.DescriptorGeometry(16, 16, 8, 2, 1, 9), np.zeros(36), 0),
+               1, 0.0)
+
+
+def test_window_descriptor_equals_cached_scan(golden):
+    img = golden["rgb48x40/image"]
+    st = H.build_integral_stack(H.gradient_map(H.Image(img), H.build_lut(9)))
+    for norm in ("none", "l2"):
+        g = H.DescriptorGeometry(16, 24, 8, 2, 1, 9, norm)
+        for x, y, d in H.scan_descriptors(st, g, 5):
+            assert np.array_equal(d, H.window_descriptor(st, (x, y), g))
+
+
+def test_resize_golden(golden):
+    src = golden["resize/src"]
+    for (nw, nh) in ((80, 69), (40, 33), (97, 83), (13, 7), (96, 82)):
+        out = H.resize_bilinear(H.Image(src), nw, nh)
+        assert np.array_equal(out.planes, golden[f"resize/{nw}x{nh}"])
+
+
+def test_resize_large_golden(golden):
+    big = synth.make_frame(synth.CONFIGS["c5"], 0)[:, :540, :960].copy()
+    for (nw, nh) in ((800, 450), (666, 375), (555, 312)):
+        out = H.resize_bilinear(H.Image(big), nw, nh)
+        assert O.sha256(out.planes) == str(golden[f"resize_big/{nw}x{nh}_sha"])
+
+
+def test_pyramid_scan_golden(golden):
+    img = golden["pyramid/image"]
+    g = H.DescriptorGeometry(16, 16, 8, 2, 1, 9)
+    model = H.LinearModel(g, golden["pyramid/weights"], -0.5)
+    dets = H.pyramid_scan(H.Image(img), model, 1.3, 4, float("-inf"))
+    assert np.array_equal(np.array([d.box for d in dets]), golden["pyramid/boxes"])
+    assert np.array_equal(np.array([d.scale for d in dets]), golden["pyramid/scale"])
+    np.testing.assert_allclose([d.score for d in dets], golden["pyramid/score"], rtol=0,
+                               atol=score_tol(golden["pyramid/weights"]))
+
+
+def test_native_library_is_the_one_loaded():
+    from paper_1703_06256_b200 import _native
+
+    lib = _native.load()
+    assert os.path.samefile(lib._name, _native.LIB_PATH)
