@@ -24,10 +24,11 @@
  *                                 bm_pitch % 4 == 0, bm_pitch >= round_up(w, 4)
  *   planes  int32  [n][bins][h+1][w+1]
  *                                 elem (f,b,Y,X) = pl[f*pl_fstride + b*pl_nstride + Y*pl_pitch + X]
- *                                 pl_pitch >= w+1.  Fast path (16-B vector stores) when
- *                                 (pl + 1) is 16-B aligned and pl_pitch, pl_nstride, pl_fstride
- *                                 are multiples of 4 and pl_pitch >= w + 4; otherwise scalar stores.
- *                                 hog_plane_pitch(w) returns the fast-path pitch.
+ *                                 pl_pitch >= w+1.  Fast path (256-bit vector stores) when
+ *                                 (pl + 1) is 32-B aligned, pl_pitch, pl_nstride, pl_fstride
+ *                                 are multiples of 8 and pl_pitch >= round_up(w, 8) + 8
+ *                                 (the padding is then written too, so every sector is whole);
+ *                                 otherwise scalar stores.  hog_plane_pitch(w) returns that pitch.
  *   grid    int32  [n][ncy][ncx][bins]  cell histograms (CellHistogramCache.grid, descriptor.py:176-185)
  */
 #ifndef HOGB200_H
@@ -52,7 +53,7 @@ const char *hog_version(void);
 /* Text of the last error raised on the calling thread ("" if none). */
 const char *hog_last_error(void);
 
-/* Fast-path plane row pitch (elements) for width w: round_up(w + 4, 8). */
+/* Fast-path plane row pitch (elements) for width w: round_up(w, 8) + 8. */
 int64_t hog_plane_pitch(int w);
 
 /* gradient.py:95-121 (gradient_map) + gradient.py:56-72 (the table itself

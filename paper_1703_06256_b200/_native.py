@@ -11,7 +11,7 @@ import os
 from .errors import FastHogError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhogb200.so")
+LIB_PATH = os.environ.get("HOGB200_LIB") or os.path.join(_HERE, "libhogb200.so")
 
 HOG_OK, HOG_EINVAL, HOG_ECUDA = 0, 1, 2
 

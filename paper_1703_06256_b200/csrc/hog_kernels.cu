@@ -8,23 +8,26 @@
 // Design (DESIGN.md has the roofline numbers):
 //   The integral planes (4*N_b bytes per pixel) are ~90% of the compulsory
 //   HBM traffic, so every plane element is written exactly once, with
-//   16-byte coalesced stores, by k_planes.  Each warp owns a tile of R plane
-//   rows x Ws columns (4 columns per lane) and walks down it: the row prefix
-//   is a warp scan over one-hot counts packed two bins per 32-bit word
-//   (16-bit lanes; a row prefix never exceeds the width), the column prefix
-//   lives in registers.  The carries a tile needs -- the row prefix left of
-//   its strip, and the plane row above its band -- come from per-tile bin
-//   counts that k_grad_bin emits while it bins the image, scanned by three
-//   tiny kernels (k_scan_cols / k_scan_rows / k_scan_tiles).  When the scan
-//   lattice is regular, k_planes also emits the cell-histogram grid from the
-//   plane values it holds in registers (4-corner formula, descriptor.py:
-//   176-185), so the planes are never re-read.
+//   16-byte coalesced stores, by k_planes.  One warp owns a band of R plane
+//   rows of one frame and sweeps it strip by strip (4 columns per lane, 128
+//   columns per strip), walking down each strip: the row prefix is a warp
+//   scan of one-hot counts packed two bins per 32-bit word (16-bit lanes; a
+//   row prefix never exceeds the width), the column prefix lives in
+//   registers, and the row prefix left of the strip is handed from strip to
+//   strip through shared memory.  The only carry that crosses warps is the
+//   per-column count above the band: k_grad_bin counts bins per (band,
+//   column) while it bins the image, and k_scan_cols turns those counts into
+//   the column counts above every band.  When the scan lattice is regular,
+//   k_planes also emits the cell-histogram grid from the plane values it
+//   holds in registers (4-corner formula, descriptor.py:176-185), so the
+//   planes are never re-read.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -34,8 +37,9 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int LUT_SIDE = 511;
-constexpr int K_THREADS = 128;          // 4 independent warps per CTA
-constexpr int MAX_FUSED_BINS = 18;      // NW <= 9 packed words
+constexpr int K_THREADS = 128;      // 4 independent warps per CTA
+constexpr int MAX_FUSED_BINS = 18;  // NW <= 9 packed words
+constexpr int CHUNK = 128;          // k_grad_bin columns per warp (32 lanes x 4)
 
 thread_local std::string g_err;
 
@@ -59,55 +63,69 @@ int check_launch(const char *what) {
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
 // ---------------------------------------------------------------------------
-// Tile geometry shared by k_grad_bin / k_bin_counts / scans / k_planes.
+// Geometry shared by k_grad_bin / k_bin_counts / k_scan_cols / k_planes.
 struct TileGeom {
     int n, h, w, bins;
-    int R;     // plane/pixel rows per band (multiple of the lattice step when fused)
-    int Ws;    // columns per strip (<= 128, multiple of 8)
-    int ns;    // strips per frame
-    int nb1;   // pixel bands: ceil(h / R)
-    int nb2;   // plane bands: h / R + 1   (plane rows 0..h)
-    int Wc;    // ns * Ws  (padded width of the per-column scratch arrays)
-    int NWB;   // u8-packed words per column count  = ceil(bins / 4)
-    int NW;    // u16-packed words per row count    = ceil(bins / 2)
-    int NWp;   // NW padded to a multiple of 4 (16-byte rows)
-    int NBp4;  // bins padded to a multiple of 4 (int32 tile carries)
+    int R;      // rows per band (multiple of the lattice step when the grid is fused)
+    int Ws;     // plane columns per k_planes strip (<= 128, multiple of 8)
+    int ns;     // strips per frame
+    int nb1;    // pixel bands: ceil(h / R)         (k_grad_bin tiles)
+    int nb2;    // plane bands: h / R + 1            (k_planes tiles; plane rows 0..h)
+    int nc1;    // 128-column chunks: ceil(w / 128)  (k_grad_bin tiles)
+    int Wc;     // nc1 * 128: padded width of the per-column scratch arrays
+    int NWB;    // u8x4 words per column count   = ceil(bins / 4)
+    int NW;     // u16x2 words per row count     = ceil(bins / 2)
+    int NWp;    // NW padded to a multiple of 4 (16-byte V rows)
+    int halo;   // extra rows a band computes for straddling cells (cell - step)
+    int Lrows;  // rows of row-carry state (R + halo)
+    int VC;     // plane columns per lane in k_planes (8: 256-bit stores, 4: 128-bit)
+    int NWARP;  // warps (strips) per k_planes CTA
+    int nss;    // super-strips: ceil(ns / NWARP)
 };
 
 // Scratch arrays (device), carved from the caller's scratch buffer.
 struct Scratch {
-    uint32_t *C;   // [n][nb1][Wc][NWB]   per-band column counts, u8 x4 packed
-    uint32_t *S;   // [n][ns][h][NWp]     per-strip row counts, u16 x2 packed
-    uint32_t *tt;  // [n][nb1][ns][NWp]   per-tile totals, u16 x2 packed
-    uint32_t *V;   // [n][nb2][Wc][NWp]   column counts above each band, u16 x2
-    uint32_t *L;   // [n][ns][h][NWp]     row counts left of each strip, u16 x2
-    int32_t *T;    // [n][nb2][ns][NBp4]  count in [0,band top) x [0,strip left)
+    uint32_t *C;  // [n][nb1][Wc][NWB]  bin counts per (pixel band, column), u8x4
+    uint32_t *V;  // [n][nb2][Wc][NWp]  counts above each plane band, u16x2
 };
 
-TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int cell) {
+TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int cell, bool v8ok) {
     TileGeom g{};
     g.n = n; g.h = h; g.w = w; g.bins = bins;
+    g.NWB = (bins + 3) / 4;
+    g.NW = (bins + 1) / 2;
+    g.NWp = (int)round_up(g.NW, 4);
+    // 8 columns per lane only when every lattice column starts a lane chunk
+    g.VC = (v8ok && g.NW <= 5 && (!fused || stride % 8 == 0)) ? 8 : 4;
+    const int span = 32 * g.VC;
     if (fused) {
         int a = 8, b = stride;
         while (b) { int r = a % b; a = b; b = r; }
         const int l = 8 / a * stride;  // lcm(8, stride): strips start on lattice columns, 32-B aligned
-        g.Ws = ((128 + stride - cell) / l) * l;
+        g.Ws = ((span + stride - cell) / l) * l;
+        g.halo = cell - stride;
     } else {
-        g.Ws = 128;
+        g.Ws = span;
+        g.halo = 0;
     }
-    g.ns = (int)((w + g.Ws - 1) / g.Ws);
-    g.Wc = g.ns * g.Ws;
+    g.ns = (w + g.Ws - 1) / g.Ws;
+    g.NWARP = g.ns < 8 ? g.ns : 8;
+    g.nss = (g.ns + g.NWARP - 1) / g.NWARP;
+    g.nc1 = (w + CHUNK - 1) / CHUNK;
+    g.Wc = g.nc1 * CHUNK;
     int R = 128;
-    auto tiles = [&](int r) { return (int64_t)n * (h / r + 1) * g.ns; };
-    while (R > 16 && tiles(R) < 148 * 64) R /= 2;
+    const char *env = getenv("HOGB200_BAND_ROWS");
+    if (env && atoi(env) >= 8) {
+        R = atoi(env);
+    } else {
+        while (R > 16 && (int64_t)n * (h / R + 1) * g.NWARP < 148 * 32) R /= 2;
+    }
     if (fused && R % stride != 0) R = (int)round_up(R, stride);
+    if (R > 240) R = 240;  // u8 column counts; packed strip-local sums stay < 2^16
     g.R = R;
     g.nb1 = (h + R - 1) / R;
     g.nb2 = h / R + 1;
-    g.NWB = (bins + 3) / 4;
-    g.NW = (bins + 1) / 2;
-    g.NWp = (int)round_up(g.NW, 4);
-    g.NBp4 = (int)round_up(bins, 4);
+    g.Lrows = R + g.halo;
     return g;
 }
 
@@ -119,19 +137,11 @@ size_t carve(const TileGeom &g, void *base, Scratch *sc) {
         return o;
     };
     size_t oC = take(sizeof(uint32_t) * (size_t)g.n * g.nb1 * g.Wc * g.NWB);
-    size_t oS = take(sizeof(uint32_t) * (size_t)g.n * g.ns * g.h * g.NWp);
-    size_t ot = take(sizeof(uint32_t) * (size_t)g.n * g.nb1 * g.ns * g.NWp);
     size_t oV = take(sizeof(uint32_t) * (size_t)g.n * g.nb2 * g.Wc * g.NWp);
-    size_t oL = take(sizeof(uint32_t) * (size_t)g.n * g.ns * g.h * g.NWp);
-    size_t oT = take(sizeof(int32_t) * (size_t)g.n * g.nb2 * g.ns * g.NBp4);
     if (sc && base) {
         char *b = (char *)base;
         sc->C = (uint32_t *)(b + oC);
-        sc->S = (uint32_t *)(b + oS);
-        sc->tt = (uint32_t *)(b + ot);
         sc->V = (uint32_t *)(b + oV);
-        sc->L = (uint32_t *)(b + oL);
-        sc->T = (int32_t *)(b + oT);
     }
     return off;
 }
@@ -148,18 +158,6 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
     return v;
 }
 
-__device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
-    return v;
-}
-
-// one-hot of bin `b` in the u16x2-packed word `w` (bins 2w, 2w+1); NO_BIN
-// (0xFF) and out-of-range values hit no word.
-__device__ __forceinline__ uint32_t oh16(uint32_t hb, uint32_t one, int w) {
-    return hb == (uint32_t)w ? one : 0u;
-}
-
 __device__ __forceinline__ uint32_t byte_of(uint32_t v, int k) { return (v >> (8 * k)) & 0xffu; }
 
 // u8x4 word -> u16x2 word holding bytes (2h, 2h+1)
@@ -171,222 +169,173 @@ __device__ __forceinline__ uint32_t half16(uint32_t v, int h) {
     return h == 0 ? (v & 0xffffu) : (v >> 16);
 }
 
-struct TileId {
-    int f, b, s;
-};
-
-__device__ __forceinline__ bool decode_tile(const TileGeom &g, int nbands, TileId &t) {
-    const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int64_t ntiles = (int64_t)g.n * nbands * g.ns;
-    if (wid >= ntiles) return false;
-    t.s = (int)(wid % g.ns);
-    const int64_t q = wid / g.ns;
-    t.b = (int)(q % nbands);
-    t.f = (int)(q / nbands);
-    return true;
+__device__ __forceinline__ int64_t warp_id() {
+    return (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
 }
 
-// Accumulates one row of bins (4 bytes per lane, 0xFF = none) into the
-// per-lane column counts (u8x4 packed) and returns the lane's row count
-// (u16x2 packed words), bins < 2*NW.
-template <int NWB, int NW>
-__device__ __forceinline__ void count_row(uint32_t bins4, uint32_t (&cc)[4][NWB],
-                                          uint32_t (&rc)[NW]) {
-#pragma unroll
-    for (int w = 0; w < NW; ++w) rc[w] = 0;
+// Per-lane column counts of 4 pixel bins (bytes of `bins4`, 0xFF = none):
+// cc[k][w] holds bins 4w..4w+3 of column k as u8x4.
+template <int NWB>
+__device__ __forceinline__ void count_cols(uint32_t bins4, uint32_t (&cc)[4][NWB]) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        uint32_t v = byte_of(bins4, k);
-        uint32_t q8 = v >> 2, one8 = 1u << ((v & 3u) << 3);
-        uint32_t q16 = v >> 1, one16 = 1u << ((v & 1u) << 4);
+        const uint32_t v = byte_of(bins4, k);
+        const uint32_t q = v >> 2, one = 1u << ((v & 3u) << 3);
 #pragma unroll
-        for (int w = 0; w < NWB; ++w) cc[k][w] += (q8 == (uint32_t)w) ? one8 : 0u;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) rc[w] += (q16 == (uint32_t)w) ? one16 : 0u;
+        for (int w = 0; w < NWB; ++w)
+            if (q == (uint32_t)w) cc[k][w] += one;
     }
 }
 
-// Per-row / per-band count outputs shared by both count producers.
-template <int NWB, int NW>
-__device__ __forceinline__ void emit_row_counts(const TileGeom &g, const Scratch &sc,
-                                                const TileId &t, int y, int lane,
-                                                uint32_t (&rc)[NW], uint32_t (&tt)[NW]) {
-    uint32_t mine = 0;
+template <int NWB>
+__device__ __forceinline__ void store_cols(const TileGeom &g, const Scratch &sc, int f, int b,
+                                           int x, uint32_t (&cc)[4][NWB]) {
+    uint32_t *cp = sc.C + (((int64_t)f * g.nb1 + b) * g.Wc + x) * NWB;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        uint32_t tot = warp_sum(rc[w]);
-        tt[w] += tot;
-        if (lane == w) mine = tot;
-    }
-    if (lane < g.NWp)
-        sc.S[(((int64_t)t.f * g.ns + t.s) * g.h + y) * g.NWp + lane] = lane < NW ? mine : 0u;
-}
-
-template <int NWB, int NW>
-__device__ __forceinline__ void emit_band_counts(const TileGeom &g, const Scratch &sc,
-                                                 const TileId &t, int x, int lane, bool own,
-                                                 uint32_t (&cc)[4][NWB], uint32_t (&tt)[NW]) {
-    if (own) {
-        uint32_t *cp = sc.C + (((int64_t)t.f * g.nb1 + t.b) * g.Wc + x) * NWB;
+    for (int k = 0; k < 4; ++k)
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int w = 0; w < NWB; ++w) cp[k * NWB + w] = cc[k][w];
-    }
-    uint32_t mine = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w)
-        if (lane == w) mine = tt[w];
-    if (lane < g.NWp)
-        sc.tt[(((int64_t)t.f * g.nb1 + t.b) * g.ns + t.s) * g.NWp + lane] = lane < NW ? mine : 0u;
+        for (int w = 0; w < NWB; ++w) cp[k * NWB + w] = cc[k][w];
 }
 
 // ---------------------------------------------------------------------------
-// K1: gradient + LUT binning (gradient.py:95-121), optionally emitting the
-// per-tile counts the plane kernel needs.  One warp = one tile of R rows x
-// Ws columns; lane L owns pixel columns xs+4L .. xs+4L+3 and slides a
-// three-row window down the band (each image row is loaded once per tile,
-// left/right neighbours come from adjacent lanes by shuffle).
+// K1: gradient + LUT binning (gradient.py:95-121), optionally counting bins
+// per (band, column) for k_scan_cols.  One warp = R rows x 128 columns of
+// one frame; lane L owns pixel columns x0+4L .. x0+4L+3 and slides a
+// three-row window down the band, two rows of loads in flight; left/right
+// neighbours come from the adjacent lanes by shuffle.
 
-template <int CH, int NWB, int NW, bool COUNTS>
+template <int CH, int NWB, bool COUNTS>
 __global__ void __launch_bounds__(K_THREADS)
 k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs,
            const uint8_t *__restrict__ lut, int8_t *__restrict__ bm, int64_t bp, int64_t bfs,
            TileGeom g, Scratch sc) {
-    TileId t;
-    if (!decode_tile(g, g.nb1, t)) return;
+    const int64_t wid = warp_id();
+    if (wid >= (int64_t)g.n * g.nb1 * g.nc1) return;
+    const int chunk = (int)(wid % g.nc1);
+    const int b = (int)((wid / g.nc1) % g.nb1);
+    const int f = (int)(wid / ((int64_t)g.nc1 * g.nb1));
     const int lane = threadIdx.x & 31;
-    const int xs = t.s * g.Ws;
-    const int x = xs + 4 * lane;
-    const bool own = 4 * lane < g.Ws;
+    const int x = chunk * CHUNK + 4 * lane;
     const bool inx = x < g.w;
-    const int y0 = t.b * g.R, y1 = min(y0 + g.R, g.h);
-    const uint8_t *im = img + (int64_t)t.f * ifs;
-    int8_t *bmf = bm + (int64_t)t.f * bfs;
+    const int y0 = b * g.R, y1 = min(y0 + g.R, g.h);
+    const uint8_t *im = img + (int64_t)f * ifs;
+    int8_t *bmf = bm + (int64_t)f * bfs;
+
+    // bytes of this lane's 4 columns that are interior pixels (1 <= x <= w-2)
+    uint32_t valid = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (x + k >= 1 && x + k <= g.w - 2) valid |= 0xffu << (8 * k);
 
     auto ldw = [&](int y, int ch) -> uint32_t {
         return (inx && y >= 0 && y < g.h)
                    ? __ldg(reinterpret_cast<const uint32_t *>(im + ch * ics + (int64_t)y * ip + x))
                    : 0u;
     };
-    auto ldb = [&](int y, int ch, int xx) -> uint32_t {
-        return (xx >= 0 && xx < g.w && y >= 0 && y < g.h) ? (uint32_t)__ldg(im + ch * ics + (int64_t)y * ip + xx)
-                                                          : 0u;
+    // left neighbour byte of lane 0, right neighbour byte of lane 31
+    auto lde = [&](int y, int ch) -> uint32_t {
+        const int xx = lane == 0 ? x - 1 : x + 4;
+        return ((lane == 0 || lane == 31) && xx >= 0 && xx < g.w && y >= 0 && y < g.h)
+                   ? (uint32_t)__ldg(im + ch * ics + (int64_t)y * ip + xx)
+                   : 0u;
     };
 
-    uint32_t up[CH], mid[CH], dn[CH], ml[CH], mr[CH], dl[CH], dr[CH];
+    // rows y-1 (r0), y (r1), y+1 (r2), y+2 (r3, in flight); e1/e3: edge bytes
+    uint32_t r0[CH], r1[CH], r2[CH], r3[CH], e1[CH], e2[CH], e3[CH];
 #pragma unroll
     for (int ch = 0; ch < CH; ++ch) {
-        up[ch] = ldw(y0 - 1, ch);
-        mid[ch] = ldw(y0, ch);
-        ml[ch] = lane == 0 ? ldb(y0, ch, x - 1) : 0u;
-        mr[ch] = lane == 31 ? ldb(y0, ch, x + 4) : 0u;
+        r0[ch] = ldw(y0 - 1, ch);
+        r1[ch] = ldw(y0, ch);
+        e1[ch] = lde(y0, ch);
+        r2[ch] = ldw(y0 + 1, ch);
+        e2[ch] = lde(y0 + 1, ch);
     }
     uint32_t cc[4][NWB];
-    uint32_t tt[NW];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
 #pragma unroll
         for (int w = 0; w < NWB; ++w) cc[k][w] = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) tt[w] = 0;
 
     for (int y = y0; y < y1; ++y) {
 #pragma unroll
         for (int ch = 0; ch < CH; ++ch) {
-            dn[ch] = ldw(y + 1, ch);
-            dl[ch] = lane == 0 ? ldb(y + 1, ch, x - 1) : 0u;
-            dr[ch] = lane == 31 ? ldb(y + 1, ch, x + 4) : 0u;
+            r3[ch] = ldw(y + 2, ch);
+            e3[ch] = lde(y + 2, ch);
         }
         uint32_t bins4 = 0xffffffffu;
         if (y > 0 && y < g.h - 1) {
-            int bdx[4], bdy[4], best[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) best[k] = -1, bdx[k] = 0, bdy[k] = 0;
+            int bdx[4], bdy[4];
 #pragma unroll
             for (int ch = 0; ch < CH; ++ch) {
-                uint32_t prev3 = __shfl_up_sync(FULL, mid[ch], 1) >> 24;
-                uint32_t next0 = __shfl_down_sync(FULL, mid[ch], 1) & 0xffu;
-                uint32_t lft = lane == 0 ? ml[ch] : prev3;
-                uint32_t rgt = lane == 31 ? mr[ch] : next0;
+                const uint32_t prev = __shfl_up_sync(FULL, r1[ch], 1);
+                const uint32_t next = __shfl_down_sync(FULL, r1[ch], 1);
+                // Lw: bytes at x-1..x+2, Rw: bytes at x+1..x+4
+                const uint32_t Lw = __byte_perm(lane == 0 ? e1[ch] : prev >> 24, r1[ch], 0x6540);
+                const uint32_t Rw = __byte_perm(r1[ch], lane == 31 ? e1[ch] : next, 0x4321);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    int L = (int)(k == 0 ? lft : byte_of(mid[ch], k - 1));
-                    int Rr = (int)(k == 3 ? rgt : byte_of(mid[ch], k + 1));
-                    int dx = Rr - L;
-                    int dy = (int)byte_of(dn[ch], k) - (int)byte_of(up[ch], k);
-                    int mag = dx * dx + dy * dy;
-                    if (mag > best[k]) best[k] = mag, bdx[k] = dx, bdy[k] = dy;  // first max wins
+                    const int dx = (int)byte_of(Rw, k) - (int)byte_of(Lw, k);
+                    const int dy = (int)byte_of(r2[ch], k) - (int)byte_of(r0[ch], k);
+                    if (CH == 1) {
+                        bdx[k] = dx, bdy[k] = dy;
+                    } else {
+                        // gradient.py:113-117: largest dx^2+dy^2 wins, first channel on ties
+                        const int mag = dx * dx + dy * dy;
+                        if (ch == 0 || mag > bdx[k] * bdx[k] + bdy[k] * bdy[k]) bdx[k] = dx, bdy[k] = dy;
+                    }
                 }
             }
             bins4 = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                int xk = x + k;
-                uint32_t v = 0xffu;
-                if (xk > 0 && xk < g.w - 1) v = __ldg(lut + (bdx[k] + 255) * LUT_SIDE + (bdy[k] + 255));
-                bins4 |= v << (8 * k);
-            }
+            for (int k = 0; k < 4; ++k)
+                bins4 |= (uint32_t)__ldg(lut + (bdx[k] * LUT_SIDE + bdy[k] + (255 * LUT_SIDE + 255)))
+                         << (8 * k);
+            bins4 = (bins4 & valid) | ~valid;
         }
-        if (inx) {
-            // bytes past w are padding; keep them NO_BIN
-            if (x + 4 > g.w) bins4 |= 0xffffffffu << (8 * (g.w - x));
-            if (own) *reinterpret_cast<uint32_t *>(bmf + (int64_t)y * bp + x) = bins4;
-        }
-        if (COUNTS) {
-            uint32_t cb = (own && inx) ? bins4 : 0xffffffffu;
-            uint32_t rc[NW];
-            count_row<NWB, NW>(cb, cc, rc);
-            emit_row_counts<NWB, NW>(g, sc, t, y, lane, rc, tt);
-        }
+        if (inx) *reinterpret_cast<uint32_t *>(bmf + (int64_t)y * bp + x) = bins4;
+        if (COUNTS) count_cols<NWB>(bins4, cc);
 #pragma unroll
         for (int ch = 0; ch < CH; ++ch) {
-            up[ch] = mid[ch];
-            mid[ch] = dn[ch];
-            ml[ch] = dl[ch];
-            mr[ch] = dr[ch];
+            r0[ch] = r1[ch];
+            r1[ch] = r2[ch];
+            r2[ch] = r3[ch];
+            e1[ch] = e2[ch];
+            e2[ch] = e3[ch];
         }
     }
-    if (COUNTS) emit_band_counts<NWB, NW>(g, sc, t, x, lane, own, cc, tt);
+    if (COUNTS) store_cols<NWB>(g, sc, f, b, x, cc);
 }
 
-// K1': the same per-tile counts from an existing bin map (hog_integral).
-template <int NWB, int NW>
+// K1': the same per-(band, column) counts from an existing bin map (hog_integral).
+template <int NWB>
 __global__ void __launch_bounds__(K_THREADS)
 k_bin_counts(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, TileGeom g, Scratch sc) {
-    TileId t;
-    if (!decode_tile(g, g.nb1, t)) return;
+    const int64_t wid = warp_id();
+    if (wid >= (int64_t)g.n * g.nb1 * g.nc1) return;
+    const int chunk = (int)(wid % g.nc1);
+    const int b = (int)((wid / g.nc1) % g.nb1);
+    const int f = (int)(wid / ((int64_t)g.nc1 * g.nb1));
     const int lane = threadIdx.x & 31;
-    const int x = t.s * g.Ws + 4 * lane;
-    const bool own = 4 * lane < g.Ws;
-    const bool inx = x < g.w;
-    const int y0 = t.b * g.R, y1 = min(y0 + g.R, g.h);
-    const int8_t *bmf = bm + (int64_t)t.f * bfs;
+    const int x = chunk * CHUNK + 4 * lane;
+    const int y0 = b * g.R, y1 = min(y0 + g.R, g.h);
+    const int8_t *bmf = bm + (int64_t)f * bfs;
+    uint32_t mask = 0;  // bytes past w count nowhere
+    if (x + 4 > g.w) mask = x >= g.w ? 0xffffffffu : 0xffffffffu << (8 * (g.w - x));
     uint32_t cc[4][NWB];
-    uint32_t tt[NW];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
 #pragma unroll
         for (int w = 0; w < NWB; ++w) cc[k][w] = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) tt[w] = 0;
     for (int y = y0; y < y1; ++y) {
         uint32_t v = 0xffffffffu;
-        if (own && inx) {
-            v = __ldg(reinterpret_cast<const uint32_t *>(bmf + (int64_t)y * bp + x));
-            if (x + 4 > g.w) v |= 0xffffffffu << (8 * (g.w - x));
-        }
-        uint32_t rc[NW];
-        count_row<NWB, NW>(v, cc, rc);
-        emit_row_counts<NWB, NW>(g, sc, t, y, lane, rc, tt);
+        if (x < g.w) v = __ldg(reinterpret_cast<const uint32_t *>(bmf + (int64_t)y * bp + x)) | mask;
+        count_cols<NWB>(v, cc);
     }
-    emit_band_counts<NWB, NW>(g, sc, t, x, lane, own, cc, tt);
+    store_cols<NWB>(g, sc, f, b, x, cc);
 }
 
-// ---------------------------------------------------------------------------
-// Carry scans (tiny: O(N_b / R + N_b / Ws) words per pixel).
-
-// V[f][b][x] = sum over bands b' < b of C[f][b'][x]  (column counts above band b)
+// V[f][b][x] = sum over pixel bands b' < b of C[f][b'][x]: column counts of
+// plane rows [0, b*R), u16x2 packed (<= h < 65536).
 template <int NWB, int NW>
 __global__ void k_scan_cols(TileGeom g, Scratch sc) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -411,59 +360,29 @@ __global__ void k_scan_cols(TileGeom g, Scratch sc) {
     }
 }
 
-// L[f][s][y] = sum over strips s' < s of S[f][s'][y]  (row counts left of strip s)
-template <int NW>
-__global__ void k_scan_rows(TileGeom g, Scratch sc) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)g.n * g.h) return;
-    const int f = (int)(i / g.h), y = (int)(i % g.h);
-    uint32_t run[NW];
-#pragma unroll
-    for (int w = 0; w < NW; ++w) run[w] = 0;
-    for (int s = 0; s < g.ns; ++s) {
-        const int64_t o = (((int64_t)f * g.ns + s) * g.h + y) * g.NWp;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            uint32_t v = sc.S[o + w];
-            sc.L[o + w] = run[w];
-            run[w] += v;
-        }
-        for (int w = NW; w < g.NWp; ++w) sc.L[o + w] = 0;
-    }
-}
-
-// T[f][b][s][n] = count of bin n in plane rows [0, b*R) x columns [0, s*Ws)
-__global__ void k_scan_tiles(TileGeom g, Scratch sc) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)g.n * g.ns * g.NBp4) return;
-    const int n = (int)(i % g.NBp4);
-    const int s = (int)((i / g.NBp4) % g.ns);
-    const int f = (int)(i / ((int64_t)g.NBp4 * g.ns));
-    uint32_t acc = 0;
-    for (int b = 0; b < g.nb2; ++b) {
-        sc.T[(((int64_t)f * g.nb2 + b) * g.ns + s) * g.NBp4 + n] = n < g.bins ? (int32_t)acc : 0;
-        if (b < g.nb1 && n < g.bins) {
-            const uint32_t *tp = sc.tt + (((int64_t)f * g.nb1 + b) * g.ns) * g.NWp + (n >> 1);
-            for (int q = 0; q < s; ++q) acc += half16(tp[(int64_t)q * g.NWp], n & 1);
-        }
-    }
-}
-
 // ---------------------------------------------------------------------------
 // K2: integral planes (+ fused cell grid).  integral.py:58-87,
-// descriptor.py:176-185.  KR = cell / lattice step (0: no grid).
+// descriptor.py:176-185.  KR = cell / lattice step (0: no grid); VC = plane
+// columns per lane (8: one 256-bit store per plane row, 4: 128-bit).
 //
-// Lane L holds P(Y, X) for X = xs+4L+1 .. xs+4L+4 and all bins in registers
-// (acc), plus P(Y, xs) in pedge.  Going from plane row Y to Y+1 adds the row
-// prefix R(Y, X) = L(Y) + (warp-exclusive count) + (lane-local count).
-// Lattice row Yl (Yl % s == 0): Hd(Yl, xi) = P(Yl, xi + cell) - P(Yl, xi)
-// is formed by shuffles, and the cell with top-left (Yl - cell, xi) is
-// Hd(Yl) - Hd(Yl - cell), kept in a KR-deep ring.
+// CTA = (frame f, band b): plane rows [Y0, Y0+R) (+ `halo` rows computed for
+// cells straddling the band).  Its NWARP warps own adjacent column strips and
+// walk the band's rows together, so every plane row leaves the SM as one
+// contiguous burst (HBM write efficiency: tools/probe_store.cu).  In a strip,
+// lane L holds P(Y, X) for its VC columns and every bin in registers (acc).
+// Row Y -> Y+1 adds the row prefix R(Y, X) = Lc(Y) + (warp-exclusive count) +
+// (lane-local count); Lc(Y), the count left of the strip, is the sum of the
+// strip totals of the warps to the left, exchanged through shared memory once
+// per group of G rows (phase A: warp scans + strip totals, barrier, phase B:
+// accumulate + store).  Frames wider than NWARP strips are swept in
+// super-strips, carrying Lc through shared memory.  Lattice row Yl:
+// Hd(Yl, xi) = P(Yl, xi + cell) - P(Yl, xi) by shuffles, and the cell with
+// top-left (Yl - cell, xi) is Hd(Yl) - Hd(Yl - cell) (per-lane ring in smem).
 
 struct PlaneOut {
     int32_t *pl;
     int64_t pp, pns, pfs;
-    int vec;
+    int vec;  // 32-B aligned rows: vector stores + full-sector padding writes
 };
 
 struct GridOut {
@@ -471,186 +390,359 @@ struct GridOut {
     int s, cell, ncx, ncy;
 };
 
-template <int NW, int KR>
-__global__ void __launch_bounds__(K_THREADS)
-k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, GridOut go,
-         TileGeom g, Scratch sc) {
-    TileId t;
-    if (!decode_tile(g, g.nb2, t)) return;
-    const int lane = threadIdx.x & 31;
-    const int xs = t.s * g.Ws;
-    const int x = xs + 4 * lane;  // pixel column of this lane's first column; P column x+1
-    const bool own = 4 * lane < g.Ws;
-    const int X0 = x + 1;
-    const int Y0 = t.b * g.R;
-    const int Ystore = min(Y0 + g.R - 1, g.h);
-    int Ycomp = Ystore;
-    if (KR) Ycomp = max(Ystore, min(Y0 + g.R - go.s + go.cell, g.h));
-    const bool st = own && X0 <= g.w;
-    const int bins = g.bins;
-    const int8_t *bmf = bm + (int64_t)t.f * bfs;
-    int32_t *plf = po.pl + (int64_t)t.f * po.pfs;
+constexpr int K2_G = 4;  // rows per phase-A/phase-B group
 
-    uint32_t acc[2 * NW][4];
-    uint32_t pedge[2 * NW];
-    if (t.b == 0) {
-#pragma unroll
-        for (int n = 0; n < 2 * NW; ++n) {
-            pedge[n] = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) acc[n][k] = 0;
+// shared-memory carve-up of one k_planes CTA (32-bit words, every array 16-B aligned)
+struct K2Smem {
+    int rowtot, Lsup, vtot, Tsup, ptop, ring, total;
+};
+
+__host__ __device__ inline int k2_r4(int v) { return (v + 3) & ~3; }
+
+__host__ __device__ inline K2Smem k2_smem(const TileGeom &g, int kr) {
+    const int NB = 2 * g.NW;
+    K2Smem m;
+    m.rowtot = 0;                                                // [2][G][NWARP][NWp]
+    m.Lsup = m.rowtot + k2_r4(2 * K2_G * g.NWARP * g.NWp);       // [2][Lrows][NWp]
+    m.vtot = m.Lsup + k2_r4(2 * g.Lrows * g.NWp);                // [NWARP][NB]
+    m.Tsup = m.vtot + k2_r4(g.NWARP * NB);                       // [2][NB]
+    m.ptop = m.Tsup + k2_r4(2 * NB);                             // [NWARP][NB][32][VC]
+    m.ring = m.ptop + k2_r4(g.NWARP * NB * 32 * g.VC);           // [NWARP][KR][NB][32]
+    m.total = m.ring + k2_r4(g.NWARP * kr * NB * 32);
+    return m;
+}
+
+__host__ __device__ inline int k2_smem_words(const TileGeom &g, int kr) { return k2_smem(g, kr).total; }
+
+template <int VC>
+__device__ __forceinline__ void store_chunk(int32_t *p, const uint32_t (&v)[VC], bool vec, int valid) {
+    if (vec) {
+        if constexpr (VC == 8) {
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]),
+                         "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                         : "memory");
+        } else {
+            *reinterpret_cast<int4 *>(p) = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
         }
     } else {
-        // top row of the band: P(Y0, X) = T + sum_{xs <= x' < X} V(x')
-        uint32_t v[4][NW];
-        const bool xin = x < g.Wc;
-        const uint32_t *vp = sc.V + (((int64_t)t.f * g.nb2 + t.b) * g.Wc + x) * g.NWp;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int w = 0; w < NW; ++w) v[k][w] = xin ? vp[k * g.NWp + w] : 0u;
-        const int32_t *tp = sc.T + (((int64_t)t.f * g.nb2 + t.b) * g.ns + t.s) * g.NBp4;
-#pragma unroll
-        for (int n = 0; n < 2 * NW; ++n) {
-            const int w = n >> 1, h = n & 1;
-            uint32_t c0 = half16(v[0][w], h), c1 = half16(v[1][w], h);
-            uint32_t c2 = half16(v[2][w], h), c3 = half16(v[3][w], h);
-            uint32_t tot = c0 + c1 + c2 + c3;
-            uint32_t inc = warp_incl_scan(tot, lane);
-            uint32_t t0 = n < bins ? (uint32_t)tp[n] : 0u;
-            uint32_t run = t0 + inc - tot;
-            acc[n][0] = (run += c0);
-            acc[n][1] = (run += c1);
-            acc[n][2] = (run += c2);
-            acc[n][3] = (run += c3);
-            pedge[n] = t0;
-        }
+        for (int k = 0; k < VC; ++k)
+            if (k < valid) p[k] = (int)v[k];
     }
+}
 
-    auto store_row = [&](int Y) {
-        int32_t *rp = plf + (int64_t)Y * po.pp;
-        if (t.s == 0 && lane == 0) {
+template <int VC>
+struct BmWord;
+template <>
+struct BmWord<4> {
+    uint32_t w;
+    __device__ __forceinline__ uint32_t byte(int k) const { return byte_of(w, k); }
+};
+template <>
+struct BmWord<8> {
+    uint32_t lo, hi;
+    __device__ __forceinline__ uint32_t byte(int k) const { return k < 4 ? byte_of(lo, k) : byte_of(hi, k - 4); }
+};
+
+// P(Y, X) = ptop(X) + Lacc(Y) + Q(Y, X):
+//   ptop(X) = sum_{xs <= x' < X} V(x')  -- band's top row relative to the strip's
+//             left edge; constant through the band, kept in shared memory
+//   Lacc(Y) = P(Y, xs)                  -- one value per bin, uniform over the warp
+//   Q(Y, X) = sum_{Y0 <= y < Y} count of row y in [xs, X)  -- <= (R+halo)*32*VC < 2^16,
+//             so two bins share one register (u16x2) and a row update is one add
+#ifndef K2_MINB
+#define K2_MINB 2
+#endif
+template <int NW, int KR, int VC, bool VEC>
+__global__ void __launch_bounds__(256, K2_MINB)
+k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, GridOut go,
+         TileGeom g, Scratch sc) {
+    extern __shared__ uint32_t smem[];
+    constexpr int NB = 2 * NW;
+    constexpr int G = K2_G;
+    const int nwarp = g.NWARP;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = (int)(blockIdx.x % g.nb2);
+    const int f = (int)(blockIdx.x / g.nb2);
+    const K2Smem lay = k2_smem(g, KR);
+    uint32_t *rowtot = smem + lay.rowtot;                    // [2][G][nwarp][NWp]
+    uint32_t *Lsup = smem + lay.Lsup;                        // [2][Lrows][NWp]
+    uint32_t *vtot = smem + lay.vtot;                        // [nwarp][NB]
+    uint32_t *Tsup = smem + lay.Tsup;                        // [2][NB]
+    uint32_t *ptop = smem + lay.ptop + (warp * NB * 32 + lane) * VC;  // this lane's [NB][VC] (stride 32*VC)
+    uint32_t *ring = smem + lay.ring + warp * KR * NB * 32 + lane;    // this lane's [KR][NB] (stride 32)
+
+    const int Y0 = b * g.R;
+    const int Ystore = min(Y0 + g.R - 1, g.h);
+    const int Ycomp = KR ? max(Ystore, min(Y0 + g.R + g.halo, g.h)) : Ystore;
+    const bool odd = (g.bins & 1) != 0;  // the last packed bin is padding
+    const int lo = g.Ws / VC - 1;        // last lane owning strip columns
+    const int NWp = g.NWp;
+    const int64_t pns = po.pns, pp = po.pp;
+    const int8_t *bmf = bm + (int64_t)f * bfs;
+    int32_t *plf = po.pl + (int64_t)f * po.pfs;
+    const uint32_t *Vb = sc.V + ((int64_t)f * g.nb2 + b) * g.Wc * NWp;
+    // lattice bookkeeping (integer divisions once per CTA)
+    const int ls = KR ? go.s : 1;
+    const int dR = KR ? go.cell / VC - 1 : 0;  // lanes between a cell's left and right corner
+    const int jtop = Y0 / ls;                   // grid row of the band's first owned cell
+    const int jend = KR ? min((Y0 + g.R - 1) / ls, go.ncy - 1) : -1;  // last owned grid row
+    const int lag = KR ? go.cell / ls : 0;      // lattice rows between a cell's top and bottom
+
+    for (int ss = 0; ss < g.nss; ++ss) {
+        const int s = ss * nwarp + warp;
+        const bool active = s < g.ns;
+        const bool last_warp = warp == nwarp - 1;
+        const int xs = s * g.Ws;
+        const int x = xs + VC * lane;  // pixel column of the lane's first column; P column x+1
+        const bool own = VC * lane < g.Ws;
+        const int X0 = x + 1;
+        const bool st = active && own && X0 <= g.w;
+        const bool lat_lane = KR && st && (x % ls) == 0 && x <= (go.ncx - 1) * ls;
+        const int gcol = x / ls;
+        const uint32_t *rdL = Lsup + (ss & 1) * g.Lrows * NWp;
+        uint32_t *wrL = Lsup + ((ss & 1) ^ 1) * g.Lrows * NWp;
+
+        uint32_t Q[NW][VC];
+        uint32_t Lacc[NB];
 #pragma unroll
-            for (int n = 0; n < 2 * NW; ++n)
-                if (n < bins) rp[(int64_t)n * po.pns] = 0;  // padded column X = 0
-        }
-        if (!st) return;
-        rp += X0;
+        for (int w = 0; w < NW; ++w)
 #pragma unroll
-        for (int n = 0; n < 2 * NW; ++n) {
-            if (n < bins) {
-                int32_t *p = rp + (int64_t)n * po.pns;
-                if (po.vec) {
-                    *reinterpret_cast<int4 *>(p) =
-                        make_int4((int)acc[n][0], (int)acc[n][1], (int)acc[n][2], (int)acc[n][3]);
-                } else {
+            for (int k = 0; k < VC; ++k) Q[w][k] = 0;
+
+        // ---- top row: ptop(X) = sum_{xs <= x' < X} V(x'); strip totals -> left edge
+        if (active) {
+            const bool vin = b > 0 && x < g.Wc;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (X0 + k <= g.w) p[k] = (int)acc[n][k];
+            for (int w = 0; w < NW; ++w) {
+                uint32_t v[VC];
+#pragma unroll
+                for (int k = 0; k < VC; ++k) v[k] = vin ? Vb[(int64_t)(x + k) * NWp + w] : 0u;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int n = 2 * w + h;
+                    uint32_t tot = 0;
+#pragma unroll
+                    for (int k = 0; k < VC; ++k) tot += half16(v[k], h);
+                    const uint32_t inc = warp_incl_scan(tot, lane);
+                    uint32_t run = inc - tot;
+                    uint32_t pt[VC];
+#pragma unroll
+                    for (int k = 0; k < VC; ++k) pt[k] = (run += half16(v[k], h));
+#pragma unroll
+                    for (int k = 0; k < VC; k += 4)
+                        *reinterpret_cast<uint4 *>(ptop + n * 32 * VC + k) =
+                            make_uint4(pt[k], pt[k + 1], pt[k + 2], pt[k + 3]);
+                    const uint32_t stot = __shfl_sync(FULL, inc, lo);  // strip total (own lanes)
+                    if (lane == 0) vtot[warp * NB + n] = stot;
                 }
             }
         }
-    };
-
-    // fused cell grid state
-    uint32_t ring[KR > 0 ? KR : 1][2 * NW];
-    const int dR = KR ? go.cell / 4 - 1 : 0;
-    const bool lat_lane = KR && own && (x % (KR ? go.s : 1)) == 0 && x <= (go.ncx - 1) * go.s;
-    auto lattice = [&](int Yl) {
-        const int yt = Yl - go.cell;
-        const bool emit = lat_lane && yt >= Y0 && yt < Y0 + g.R && yt <= (go.ncy - 1) * go.s;
-        uint32_t gv[2 * NW];
+        __syncthreads();
+        if (active) {
 #pragma unroll
-        for (int n = 0; n < 2 * NW; ++n) {
-            uint32_t r = __shfl_down_sync(FULL, acc[n][3], dR);
-            uint32_t l = __shfl_up_sync(FULL, acc[n][3], 1);
-            if (lane == 0) l = pedge[n];
-            uint32_t hcur = r - l;
-            gv[n] = hcur - ring[0][n];
+            for (int n = 0; n < NB; ++n) {
+                uint32_t T = ss ? Tsup[(ss & 1) * NB + n] : 0u;
 #pragma unroll
-            for (int q = 0; q + 1 < KR; ++q) ring[q][n] = ring[q + 1][n];
-            ring[KR > 0 ? KR - 1 : 0][n] = hcur;
-        }
-        if (emit) {
-            int32_t *gp = go.grid +
-                          (((int64_t)t.f * go.ncy + yt / go.s) * go.ncx + x / go.s) * bins;
-            if ((bins & 3) == 0) {
-#pragma unroll
-                for (int n = 0; n + 3 < 2 * NW; n += 4)
-                    if (n < bins)
-                        *reinterpret_cast<int4 *>(gp + n) =
-                            make_int4((int)gv[n], (int)gv[n + 1], (int)gv[n + 2], (int)gv[n + 3]);
-            } else {
-#pragma unroll
-                for (int n = 0; n < 2 * NW; ++n)
-                    if (n < bins) gp[n] = (int)gv[n];
+                for (int q = 0; q < 8; ++q)
+                    if (q < warp) T += vtot[q * NB + n];
+                Lacc[n] = T;  // P(Y0, xs)
             }
         }
-    };
+        if (warp == 0 && lane < NB) {  // P(Y0, .) at the next super-strip's left edge
+            uint32_t T = ss ? Tsup[(ss & 1) * NB + lane] : 0u;
+            for (int q = 0; q < nwarp; ++q)
+                if (ss * nwarp + q < g.ns) T += vtot[q * NB + lane];
+            Tsup[((ss & 1) ^ 1) * NB + lane] = T;
+        }
 
-    store_row(Y0);
-    if (KR) {
+        // plane row pointer (plane 0, the lane's first column) of the next row to store
+        int32_t *prow = plf + (int64_t)Y0 * pp + X0;
+        auto store_row = [&]() {
+            if (s == 0 && lane == 0) {
+                // padded column X = 0; on aligned rows also the previous row's tail
+                // padding, so that sector is written whole
+                int32_t *p0 = prow - X0;
 #pragma unroll
-        for (int q = 0; q < (KR > 0 ? KR : 1); ++q)
+                for (int n = 0; n < NB; ++n) {
+                    if (n < NB - 1 || !odd) {
+                        if (VEC)
+                            asm volatile("st.global.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p0 - 7),
+                                         "r"(0)
+                                         : "memory");
+                        else
+                            *p0 = 0;
+                    }
+                    p0 += pns;
+                }
+            }
+            if (st) {
+                int32_t *p = prow;
+                const int valid = g.w - X0 + 1;
 #pragma unroll
-            for (int n = 0; n < 2 * NW; ++n) ring[q][n] = 0;
-        lattice(Y0);
-    }
+                for (int n = 0; n < NB; ++n) {
+                    if (n < NB - 1 || !odd) {
+                        uint32_t vals[VC];
+#pragma unroll
+                        for (int k = 0; k < VC; k += 4) {
+                            const uint4 t4 = *reinterpret_cast<const uint4 *>(ptop + n * 32 * VC + k);
+                            vals[k] = t4.x;
+                            vals[k + 1] = t4.y;
+                            vals[k + 2] = t4.z;
+                            vals[k + 3] = t4.w;
+                        }
+#pragma unroll
+                        for (int k = 0; k < VC; ++k) vals[k] += Lacc[n] + half16(Q[n >> 1][k], n & 1);
+                        store_chunk<VC>(p, vals, VEC, valid);
+                    }
+                    p += pns;
+                }
+            }
+            prow += pp;
+        };
 
-    auto load_bm = [&](int Y) -> uint32_t {
-        if (x >= g.w) return 0xffffffffu;
-        uint32_t v = __ldg(reinterpret_cast<const uint32_t *>(bmf + (int64_t)Y * bp + x));
-        if (x + 4 > g.w) v |= 0xffffffffu << (8 * (g.w - x));
-        return v;
-    };
-    const uint32_t *Lbase = sc.L + ((int64_t)t.f * g.ns + t.s) * g.h * g.NWp;
-    uint32_t nbm = 0, nL[NW];
-    if (Y0 < Ycomp) {
-        nbm = load_bm(Y0);
+        // fused cell grid: lattice row number `li` (row Y0 + li*ls)
+        int li = 0;
+        int32_t *gptr = KR ? go.grid + (((int64_t)f * go.ncy + (jtop - lag)) * go.ncx + gcol) * g.bins : nullptr;
+        const int64_t gstep = (int64_t)go.ncx * g.bins;
+        auto lattice = [&]() {
+            const int jt = jtop - lag + li;  // grid row whose bottom edge is this lattice row
+            const bool emit = lat_lane && jt >= jtop && jt <= jend;
+            uint32_t gv[NB];
 #pragma unroll
-        for (int w = 0; w < NW; ++w) nL[w] = Lbase[(int64_t)Y0 * g.NWp + w];
-    }
-    for (int Y = Y0; Y < Ycomp; ++Y) {
-        const uint32_t b4 = nbm;
-        uint32_t Lw[NW];
+            for (int n = 0; n < NB; ++n) {
+                const uint32_t lv = ptop[n * 32 * VC + VC - 1] + Lacc[n] + half16(Q[n >> 1][VC - 1], n & 1);
+                const uint32_t r = __shfl_down_sync(FULL, lv, dR);
+                uint32_t l = __shfl_up_sync(FULL, lv, 1);
+                if (lane == 0) l = Lacc[n];
+                const uint32_t hcur = r - l;  // P(Yl, x + cell) - P(Yl, x)
+                gv[n] = hcur - ring[n * 32];
 #pragma unroll
-        for (int w = 0; w < NW; ++w) Lw[w] = nL[w];
-        if (Y + 1 < Ycomp) {
-            nbm = load_bm(Y + 1);
+                for (int q = 0; q + 1 < KR; ++q) ring[(q * NB + n) * 32] = ring[((q + 1) * NB + n) * 32];
+                ring[((KR > 0 ? KR - 1 : 0) * NB + n) * 32] = hcur;
+            }
+            if (emit) {
+                if ((g.bins & 3) == 0) {
 #pragma unroll
-            for (int w = 0; w < NW; ++w) nL[w] = Lbase[(int64_t)(Y + 1) * g.NWp + w];
+                    for (int n = 0; n + 3 < NB; n += 4)
+                        *reinterpret_cast<int4 *>(gptr + n) =
+                            make_int4((int)gv[n], (int)gv[n + 1], (int)gv[n + 2], (int)gv[n + 3]);
+                } else {
+#pragma unroll
+                    for (int n = 0; n < NB; ++n)
+                        if (n < NB - 1 || !odd) gptr[n] = (int)gv[n];
+                }
+            }
+            gptr += gstep;
+            ++li;
+        };
+
+        if (active) {
+            store_row();
+            if (KR) lattice();
         }
-        uint32_t hb[4], one[4];
+
+        const int8_t *brow = bmf + (int64_t)Y0 * bp + x;
+        const bool bin_ok = active && x < g.w;
+        const int bvalid = g.w - x;  // bytes of the lane's chunk inside the frame
+        auto load_bm = [&](int rel) -> BmWord<VC> {
+            BmWord<VC> r;
+            const bool ok = bin_ok && Y0 + rel < Ycomp;
+            if constexpr (VC == 8) {
+                uint2 v = ok ? __ldg(reinterpret_cast<const uint2 *>(brow + (int64_t)rel * bp))
+                             : make_uint2(0xffffffffu, 0xffffffffu);
+                if (bvalid < 8) {  // bytes past w count nowhere
+                    if (bvalid < 4) v.x |= 0xffffffffu << (8 * max(bvalid, 0)), v.y = 0xffffffffu;
+                    else v.y |= 0xffffffffu << (8 * (bvalid - 4));
+                }
+                r.lo = v.x;
+                r.hi = v.y;
+            } else {
+                uint32_t v = ok ? __ldg(reinterpret_cast<const uint32_t *>(brow + (int64_t)rel * bp))
+                                : 0xffffffffu;
+                if (bvalid < 4) v |= 0xffffffffu << (8 * max(bvalid, 0));
+                r.w = v;
+            }
+            return r;
+        };
+
+        BmWord<VC> nxt[G];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            uint32_t v = byte_of(b4, k);
-            hb[k] = v >> 1;
-            one[k] = 1u << ((v & 1u) << 4);
-        }
+        for (int i = 0; i < G; ++i) nxt[i] = load_bm(i);
+        int latc = ls;  // rows until the next lattice row
+        for (int rel = 0; Y0 + rel < Ycomp; rel += G) {
+            const int gp = (rel / G) & 1;
+            BmWord<VC> bw[G];
+            uint32_t ex[G][NW];
+            const uint32_t *rt_rd = rowtot + gp * G * nwarp * NWp;
+            // ---- phase A: G rows of warp scans (independent) + strip totals
+            if (active) {
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            uint32_t o0 = oh16(hb[0], one[0], w), o1 = oh16(hb[1], one[1], w);
-            uint32_t o2 = oh16(hb[2], one[2], w), o3 = oh16(hb[3], one[3], w);
-            uint32_t tot = o0 + o1 + o2 + o3;
-            uint32_t inc = warp_incl_scan(tot, lane);
-            uint32_t run = Lw[w] + inc - tot;  // row prefix at X = x (u16x2, <= width)
-            pedge[2 * w] += Lw[w] & 0xffffu;
-            pedge[2 * w + 1] += Lw[w] >> 16;
-            run += o0;
-            acc[2 * w][0] += run & 0xffffu;
-            acc[2 * w + 1][0] += run >> 16;
-            run += o1;
-            acc[2 * w][1] += run & 0xffffu;
-            acc[2 * w + 1][1] += run >> 16;
-            run += o2;
-            acc[2 * w][2] += run & 0xffffu;
-            acc[2 * w + 1][2] += run >> 16;
-            run += o3;
-            acc[2 * w][3] += run & 0xffffu;
-            acc[2 * w + 1][3] += run >> 16;
+                for (int i = 0; i < G; ++i) {
+                    bw[i] = nxt[i];
+                    nxt[i] = load_bm(rel + G + i);  // next group in flight during this one
+                }
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    uint32_t hb[VC], one[VC];
+#pragma unroll
+                    for (int k = 0; k < VC; ++k) {
+                        const uint32_t v = bw[i].byte(k);
+                        hb[k] = v >> 1;
+                        one[k] = 1u << ((v & 1u) << 4);
+                    }
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) {
+                        uint32_t tot = 0;
+#pragma unroll
+                        for (int k = 0; k < VC; ++k) tot += hb[k] == (uint32_t)w ? one[k] : 0u;
+                        const uint32_t inc = warp_incl_scan(tot, lane);
+                        ex[i][w] = inc - tot;  // strip-exclusive count
+                        const uint32_t rt = __shfl_sync(FULL, inc, lo);
+                        if (lane == 0) rowtot[((gp * G + i) * nwarp + warp) * NWp + w] = rt;
+                    }
+                }
+            }
+            __syncthreads();
+            // ---- phase B: carries, accumulate, store, lattice
+            if (active) {
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    if (Y0 + rel + i < Ycomp) {
+                        const uint32_t *rti = rt_rd + i * nwarp * NWp;
+                        uint32_t hb[VC], one[VC];
+#pragma unroll
+                        for (int k = 0; k < VC; ++k) {
+                            const uint32_t v = bw[i].byte(k);
+                            hb[k] = v >> 1;
+                            one[k] = 1u << ((v & 1u) << 4);
+                        }
+#pragma unroll
+                        for (int w = 0; w < NW; ++w) {
+                            uint32_t L = ss ? rdL[(rel + i) * NWp + w] : 0u;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                if (q < warp) L += rti[q * NWp + w];
+                            if (last_warp && lane == 0) wrL[(rel + i) * NWp + w] = L + rti[warp * NWp + w];
+                            Lacc[2 * w] += L & 0xffffu;
+                            Lacc[2 * w + 1] += L >> 16;
+                            uint32_t run = ex[i][w];
+#pragma unroll
+                            for (int k = 0; k < VC; ++k) {
+                                run += hb[k] == (uint32_t)w ? one[k] : 0u;
+                                Q[w][k] += run;
+                            }
+                        }
+                        if (Y0 + rel + i + 1 <= Ystore) store_row();
+                        if (KR && --latc == 0) {
+                            latc = ls;
+                            lattice();
+                        }
+                    }
+                }
+            }
         }
-        if (Y + 1 <= Ystore) store_row(Y + 1);
-        if (KR && ((Y + 1) % go.s) == 0) lattice(Y + 1);
+        __syncthreads();
     }
 }
 
@@ -808,69 +900,88 @@ __global__ void k_resize(const uint8_t *__restrict__ src, int n, int c, int h, i
 // ---------------------------------------------------------------------------
 // Host-side dispatch
 
-inline unsigned blocks_for_tiles(int64_t tiles) {
-    return (unsigned)((tiles + (K_THREADS / 32) - 1) / (K_THREADS / 32));
+inline unsigned blocks_for_warps(int64_t warps) {
+    return (unsigned)((warps + (K_THREADS / 32) - 1) / (K_THREADS / 32));
 }
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-template <int NW>
-void launch_counts_from_image(int c, const uint8_t *img, int64_t ip, int64_t ics, int64_t ifs,
-                              const uint8_t *lut, int8_t *bm, int64_t bp, int64_t bfs,
-                              const TileGeom &g, const Scratch &sc, cudaStream_t st, bool counts) {
-    constexpr int NWB = (2 * NW + 3) / 4;
-    const unsigned nb = blocks_for_tiles((int64_t)g.n * g.nb1 * g.ns);
+template <int NWB>
+void launch_grad_bin(int c, bool counts, const uint8_t *img, int64_t ip, int64_t ics, int64_t ifs,
+                     const uint8_t *lut, int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g,
+                     const Scratch &sc, cudaStream_t st) {
+    const unsigned nb = blocks_for_warps((int64_t)g.n * g.nb1 * g.nc1);
+#define LAUNCH(CHv, CNT) \
+    k_grad_bin<CHv, NWB, CNT><<<nb, K_THREADS, 0, st>>>(img, ip, ics, ifs, lut, bm, bp, bfs, g, sc)
     if (c == 1) {
-        if (counts)
-            k_grad_bin<1, NWB, NW, true><<<nb, K_THREADS, 0, st>>>(img, ip, ics, ifs, lut, bm, bp, bfs, g, sc);
-        else
-            k_grad_bin<1, NWB, NW, false><<<nb, K_THREADS, 0, st>>>(img, ip, ics, ifs, lut, bm, bp, bfs, g, sc);
+        if (counts) LAUNCH(1, true); else LAUNCH(1, false);
     } else {
-        if (counts)
-            k_grad_bin<3, NWB, NW, true><<<nb, K_THREADS, 0, st>>>(img, ip, ics, ifs, lut, bm, bp, bfs, g, sc);
-        else
-            k_grad_bin<3, NWB, NW, false><<<nb, K_THREADS, 0, st>>>(img, ip, ics, ifs, lut, bm, bp, bfs, g, sc);
+        if (counts) LAUNCH(3, true); else LAUNCH(3, false);
     }
+#undef LAUNCH
 }
 
 template <int NW>
-void launch_scans(const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+void launch_scan(const TileGeom &g, const Scratch &sc, cudaStream_t st) {
     constexpr int NWB = (2 * NW + 3) / 4;
     k_scan_cols<NWB, NW><<<blocks_for((int64_t)g.n * g.Wc, 256), 256, 0, st>>>(g, sc);
-    k_scan_rows<NW><<<blocks_for((int64_t)g.n * g.h, 256), 256, 0, st>>>(g, sc);
-    k_scan_tiles<<<blocks_for((int64_t)g.n * g.ns * g.NBp4, 256), 256, 0, st>>>(g, sc);
+}
+
+template <int NW, int KR, int VC, bool VEC>
+void launch_planes_vc(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                      const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+    const size_t smem = (size_t)k2_smem_words(g, KR) * 4;
+    static size_t configured = 0;  // per instantiation
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(k_planes<NW, KR, VC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        configured = smem;
+    }
+    k_planes<NW, KR, VC, VEC><<<(unsigned)((int64_t)g.n * g.nb2), 32 * g.NWARP, smem, st>>>(
+        bm, bp, bfs, po, go, g, sc);
+}
+
+template <int NW, int KR>
+void launch_planes_kr(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                      const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+    if constexpr (NW <= 5) {
+        if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true>(bm, bp, bfs, po, go, g, sc, st);
+    }
+    if (po.vec)
+        launch_planes_vc<NW, KR, 4, true>(bm, bp, bfs, po, go, g, sc, st);
+    else
+        launch_planes_vc<NW, KR, 4, false>(bm, bp, bfs, po, go, g, sc, st);
 }
 
 template <int NW>
 void launch_planes(int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
                    const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
-    const unsigned nb = blocks_for_tiles((int64_t)g.n * g.nb2 * g.ns);
     if (kr == 0)
-        k_planes<NW, 0><<<nb, K_THREADS, 0, st>>>(bm, bp, bfs, po, go, g, sc);
+        launch_planes_kr<NW, 0>(bm, bp, bfs, po, go, g, sc, st);
     else if (kr == 1)
-        k_planes<NW, 1><<<nb, K_THREADS, 0, st>>>(bm, bp, bfs, po, go, g, sc);
+        launch_planes_kr<NW, 1>(bm, bp, bfs, po, go, g, sc, st);
     else
-        k_planes<NW, 2><<<nb, K_THREADS, 0, st>>>(bm, bp, bfs, po, go, g, sc);
+        launch_planes_kr<NW, 2>(bm, bp, bfs, po, go, g, sc, st);
 }
 
 template <int NW>
 void launch_counts_from_bm(const int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g,
                            const Scratch &sc, cudaStream_t st) {
     constexpr int NWB = (2 * NW + 3) / 4;
-    k_bin_counts<NWB, NW><<<blocks_for_tiles((int64_t)g.n * g.nb1 * g.ns), K_THREADS, 0, st>>>(
+    k_bin_counts<NWB><<<blocks_for_warps((int64_t)g.n * g.nb1 * g.nc1), K_THREADS, 0, st>>>(
         bm, bp, bfs, g, sc);
 }
 
-#define HOG_SWITCH_NW(nw, CALL)                                              \
-    switch (nw) {                                                            \
-        case 1: CALL(1); break;                                              \
-        case 2: CALL(2); break;                                              \
-        case 3: CALL(3); break;                                              \
-        case 4: CALL(4); break;                                              \
-        case 5: CALL(5); break;                                              \
-        case 6: CALL(6); break;                                              \
-        case 7: CALL(7); break;                                              \
-        case 8: CALL(8); break;                                              \
-        case 9: CALL(9); break;                                              \
+#define HOG_SWITCH_NW(nw, CALL)                                                   \
+    switch (nw) {                                                                 \
+        case 1: CALL(1); break;                                                   \
+        case 2: CALL(2); break;                                                   \
+        case 3: CALL(3); break;                                                   \
+        case 4: CALL(4); break;                                                   \
+        case 5: CALL(5); break;                                                   \
+        case 6: CALL(6); break;                                                   \
+        case 7: CALL(7); break;                                                   \
+        case 8: CALL(8); break;                                                   \
+        case 9: CALL(9); break;                                                   \
         default: return fail(HOG_EINVAL, "internal: NW %d not instantiated", nw); \
     }
 
@@ -886,7 +997,7 @@ int check_bins(int bins) {
     return HOG_OK;
 }
 
-int check_pitch8(const void *p, int64_t pitch, int w, const char *what) {
+int check_pitch4(const void *p, int64_t pitch, int w, const char *what) {
     if (((uintptr_t)p & 3) != 0 || pitch % 4 != 0 || pitch < round_up(w, 4))
         return fail(HOG_EINVAL, "%s: need 4-byte aligned base and pitch %% 4 == 0, pitch >= %lld (got %lld)",
                     what, (long long)round_up(w, 4), (long long)pitch);
@@ -895,9 +1006,13 @@ int check_pitch8(const void *p, int64_t pitch, int w, const char *what) {
 
 PlaneOut make_po(int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, int w) {
     PlaneOut po{pl, pp, pns, pfs, 0};
-    po.vec = (((uintptr_t)(pl + 1) & 15) == 0) && pp % 4 == 0 && pns % 4 == 0 && pfs % 4 == 0 &&
-             pp >= (int64_t)w + 4;
+    po.vec = (((uintptr_t)(pl + 1) & 31) == 0) && pp % 8 == 0 && pns % 8 == 0 && pfs % 8 == 0 &&
+             pp >= round_up(w, 8) + 8;
     return po;
+}
+
+bool v8_ok(const PlaneOut &po, const int8_t *bm, int64_t bp, int64_t bfs) {
+    return po.vec && ((uintptr_t)bm & 7) == 0 && bp % 8 == 0 && bfs % 8 == 0;
 }
 
 int integral_impl(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w, int bins,
@@ -909,16 +1024,16 @@ int integral_impl(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w
         k_generic_cols<<<blocks_for((int64_t)n * bins * (w + 1), 128), 128, 0, st>>>(po, n, h, w, bins);
         return check_launch("integral (generic)");
     }
-    TileGeom g = make_geom(n, h, w, bins, false, 0, 0);
+    TileGeom g = make_geom(n, h, w, bins, false, 0, 0, v8_ok(po, bm, bp, bfs));
     Scratch sc{};
     size_t need = carve(g, nullptr, nullptr);
     if (scratch == nullptr || sbytes < need)
         return fail(HOG_EINVAL, "scratch too small: need %zu bytes, got %zu", need, sbytes);
     carve(g, scratch, &sc);
-    GridOut go{nullptr, 4, 4, 0, 0};
+    GridOut go{nullptr, 4, 4, 1, 1};
 #define CALL(NWv)                                       \
     launch_counts_from_bm<NWv>(bm, bp, bfs, g, sc, st); \
-    launch_scans<NWv>(g, sc, st);                       \
+    launch_scan<NWv>(g, sc, st);                        \
     launch_planes<NWv>(0, bm, bp, bfs, po, go, g, sc, st);
     HOG_SWITCH_NW(g.NW, CALL)
 #undef CALL
@@ -932,11 +1047,11 @@ int integral_impl(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w
 
 extern "C" {
 
-const char *hog_version(void) { return "hogb200 1.0 sm_100a"; }
+const char *hog_version(void) { return "hogb200 1.2 sm_100a"; }
 
 const char *hog_last_error(void) { return g_err.c_str(); }
 
-int64_t hog_plane_pitch(int w) { return round_up((int64_t)w + 4, 8); }
+int64_t hog_plane_pitch(int w) { return round_up((int64_t)w, 8) + 8; }
 
 int hog_grad_bin(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int64_t ics,
                  int64_t ifs, const uint8_t *lut, int bins, int8_t *bm, int64_t bp, int64_t bfs,
@@ -945,24 +1060,25 @@ int hog_grad_bin(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
     int e;
     if ((e = check_frames(n, h, w)) || (e = check_bins(bins))) return e;
     if (c != 1 && c != 3) return fail(HOG_EINVAL, "channels must be 1 or 3, got %d", c);
-    if ((e = check_pitch8(img, ip, w, "image")) || (e = check_pitch8(bm, bp, w, "binmap"))) return e;
+    if ((e = check_pitch4(img, ip, w, "image")) || (e = check_pitch4(bm, bp, w, "binmap"))) return e;
     if (!img || !lut || !bm) return fail(HOG_EINVAL, "null buffer");
-    TileGeom g = make_geom(n, h, w, bins, false, 0, 0);
+    TileGeom g = make_geom(n, h, w, bins, false, 0, 0, false);
     Scratch sc{};
-    cudaStream_t st = (cudaStream_t)stream;
-    // bins only affect counting; run the NW=1 instance without counts
-    launch_counts_from_image<1>(c, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st, false);
+    launch_grad_bin<1>(c, false, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, (cudaStream_t)stream);
     return check_launch("hog_grad_bin");
 }
 
 size_t hog_scratch_bytes(int n, int h, int w, int bins, int stride, int cell) {
     if (n < 1 || h < 1 || w < 1 || bins < 1) return 0;
     bool fused = stride > 0 && cell > 0;
-    TileGeom g = make_geom(n, h, w, bins, fused, stride, cell);
-    size_t a = carve(g, nullptr, nullptr);
-    TileGeom g2 = make_geom(n, h, w, bins, false, 0, 0);
-    size_t b = carve(g2, nullptr, nullptr);
-    return a > b ? a : b;
+    size_t m = 0;
+    for (int v8 = 0; v8 < 2; ++v8) {
+        size_t a = carve(make_geom(n, h, w, bins, fused, stride, cell, v8), nullptr, nullptr);
+        size_t b = carve(make_geom(n, h, w, bins, false, 0, 0, v8), nullptr, nullptr);
+        m = a > m ? a : m;
+        m = b > m ? b : m;
+    }
+    return m;
 }
 
 int hog_integral(const int8_t *bm, int n, int h, int w, int64_t bp, int64_t bfs, int bins,
@@ -971,7 +1087,7 @@ int hog_integral(const int8_t *bm, int n, int h, int w, int64_t bp, int64_t bfs,
     g_err.clear();
     int e;
     if ((e = check_frames(n, h, w)) || (e = check_bins(bins))) return e;
-    if ((e = check_pitch8(bm, bp, w, "binmap"))) return e;
+    if ((e = check_pitch4(bm, bp, w, "binmap"))) return e;
     if (pp < (int64_t)w + 1) return fail(HOG_EINVAL, "plane pitch %lld < w+1", (long long)pp);
     if (!bm || !pl) return fail(HOG_EINVAL, "null buffer");
     return integral_impl(bm, bp, bfs, n, h, w, bins, pl, pp, pns, pfs, scratch, sbytes,
@@ -987,7 +1103,7 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
     int e;
     if ((e = check_frames(n, h, w)) || (e = check_bins(bins))) return e;
     if (c != 1 && c != 3) return fail(HOG_EINVAL, "channels must be 1 or 3, got %d", c);
-    if ((e = check_pitch8(img, ip, w, "image")) || (e = check_pitch8(bm, bp, w, "binmap"))) return e;
+    if ((e = check_pitch4(img, ip, w, "image")) || (e = check_pitch4(bm, bp, w, "binmap"))) return e;
     if (pp < (int64_t)w + 1) return fail(HOG_EINVAL, "plane pitch %lld < w+1", (long long)pp);
     if (!img || !lut || !bm || !pl) return fail(HOG_EINVAL, "null buffer");
     if (bins > MAX_FUSED_BINS)
@@ -1005,24 +1121,24 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
         kr = cell / stride;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    TileGeom g = make_geom(n, h, w, bins, kr > 0, stride, cell);
+    PlaneOut po = make_po(pl, pp, pns, pfs, w);
+    TileGeom g = make_geom(n, h, w, bins, kr > 0, stride, cell, v8_ok(po, bm, bp, bfs));
     Scratch sc{};
     size_t need = carve(g, nullptr, nullptr);
     if (scratch == nullptr || sbytes < need)
         return fail(HOG_EINVAL, "scratch too small: need %zu bytes, got %zu", need, sbytes);
     carve(g, scratch, &sc);
-    PlaneOut po = make_po(pl, pp, pns, pfs, w);
-    GridOut go{grid, kr ? stride : 4, kr ? cell : 4, ncx, ncy};
+    GridOut go{grid, kr ? stride : 4, kr ? cell : 4, kr ? ncx : 1, kr ? ncy : 1};
     auto mark = [&](int i) {
         if (stage_events && stage_events[i]) cudaEventRecord((cudaEvent_t)stage_events[i], st);
     };
-#define CALL(NWv)                                                                          \
-    mark(0);                                                                               \
-    launch_counts_from_image<NWv>(c, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st, true); \
-    mark(1);                                                                               \
-    launch_scans<NWv>(g, sc, st);                                                          \
-    mark(2);                                                                               \
-    launch_planes<NWv>(kr, bm, bp, bfs, po, go, g, sc, st);                                \
+#define CALL(NWv)                                                                           \
+    mark(0);                                                                                \
+    launch_grad_bin<(2 * NWv + 3) / 4>(c, true, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st); \
+    mark(1);                                                                                \
+    launch_scan<NWv>(g, sc, st);                                                            \
+    mark(2);                                                                                \
+    launch_planes<NWv>(kr, bm, bp, bfs, po, go, g, sc, st);                                 \
     mark(3);
     HOG_SWITCH_NW(g.NW, CALL)
 #undef CALL

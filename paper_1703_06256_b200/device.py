@@ -3,12 +3,13 @@ allocations; the compute is libhogb200.so).
 
 HBM layouts (include/hogb200.h):
   frames  uint8 (N, C, H, Wp)        Wp = round_up(W, 4)   (pitched rows)
-  binmap  int8  (N, H, Wp)           -1 = NO_BIN
-  planes  int32 (N, bins, H+1, Pp)   Pp = round_up(W + 4, 8); the tensor view
+  binmap  int8  (N, H, Wb)           Wb = round_up(W, 8); -1 = NO_BIN
+  planes  int32 (N, bins, H+1, Pp)   Pp = round_up(W, 8) + 8; the tensor view
                                      starts 7 elements into its allocation so
                                      plane column 1 of every row is 32-byte
-                                     aligned and each lane's 16-B store is one
-                                     aligned half-sector.
+                                     aligned: each lane's 8 columns are one
+                                     256-bit store, and column 0 plus the
+                                     previous row's padding form one sector.
   grid    int32 (N, ncy, ncx, bins)
 """
 from __future__ import annotations
@@ -114,7 +115,7 @@ class DevBinmap:
 
 def alloc_binmap(n, h, w, device=None) -> DevBinmap:
     t = require_cuda()
-    return DevBinmap(t.empty((n, h, round_up(w, 4)), dtype=t.int8, device=device or "cuda"),
+    return DevBinmap(t.empty((n, h, round_up(w, 8)), dtype=t.int8, device=device or "cuda"),
                      n, h, w)
 
 
@@ -149,7 +150,7 @@ class DevPlanes:
 def alloc_planes(n, bins, h, w, device=None) -> DevPlanes:
     t = require_cuda()
     pitch = int(_native.load().hog_plane_pitch(w))
-    total = n * bins * (h + 1) * pitch + 8
+    total = n * bins * (h + 1) * pitch + 16
     base = t.empty(total, dtype=t.int32, device=device or "cuda")
     return DevPlanes(base, n, bins, h, w, pitch)
 
