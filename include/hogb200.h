@@ -120,6 +120,16 @@ int hog_window_features(const int32_t *grid, int n, int ncy, int ncx, int bins,
                         int norm, double eps_term, const double *weights, double bias,
                         double *scores, double *desc, hog_stream_t stream);
 
+/* detector.py:140-154 + descriptor.py:107-124 for block == 1 on a regular
+ * cell lattice: window (iy, ix) reads cells (iy + cy*k, ix + cx*k), k = cell
+ * / lattice step in {1, 2}, cells_x == 8 (64-pixel windows of 8-pixel cells).
+ *   scores[f][iy][ix] = bias + sum_{cy,cx,b} w[(cy*8 + cx)*bins + b] * v
+ * with v = grid value, or grid value / den[f][cell] (IEEE division) when den
+ * (hog_cell_norm output) is given.  fp64 accumulation. */
+int hog_scores_lattice(const int32_t *grid, const double *den, int n, int ncy, int ncx, int bins,
+                       int noy, int nox, int cells_x, int cells_y, int k, const double *weights,
+                       double bias, double *scores, hog_stream_t stream);
+
 /* detector.py:202-221 (_resize_bilinear): separable bilinear, pixel centres
  * aligned, float64 in the reference's operation order (no FMA contraction),
  * rint half-even, clip to 0..255.  ry = h / nh and rx = w / nw as computed by

@@ -816,6 +816,123 @@ __global__ void k_cell_norm(const int32_t *__restrict__ grid, int64_t ncells_tot
     den[i] = norm == 1 ? __dadd_rn(s, eps_term) : __dsqrt_rn(__dadd_rn(s, eps_term));
 }
 
+// ---------------------------------------------------------------------------
+// Window scores on a regular cell lattice (detector.py:140-154 with block = 1,
+// descriptor.py:107-124): the window at lattice origin (iy, ix) reads cells
+// (iy + cy*K, ix + cx*K), so scoring is a 2-D correlation of the cell grid
+// with the weight tensor.  fp64 throughout (SURVEY: fp32 misses 1e-5 on
+// blurred inputs).  Each thread owns SC_TY x SC_TX windows (register tile);
+// the CTA streams the grid rows it needs through shared memory as doubles
+// (normalised by the per-cell denominator when one is given: the division
+// happens once per cell, bit-exact with descriptor.py:119-124).
+constexpr int SC_TY = 4, SC_TX = 8, SC_YG = 2;  // windows per thread (y, x); warps per CTA
+constexpr int SC_COLS = 32 * SC_TX;              // window columns per CTA
+
+template <int CX>
+__global__ void __launch_bounds__(32 * SC_YG)
+k_scores_lattice(const int32_t *__restrict__ grid, const double *__restrict__ den, int ncy, int ncx,
+                 int bins, int noy, int nox, int cells_y, int K, const double *__restrict__ wts,
+                 double bias, double *__restrict__ scores) {
+    extern __shared__ double dsm[];
+    const int span = SC_COLS + (CX - 1) * K;          // grid columns a CTA touches
+    const int spad = span + span / 8 + 1;             // skewed row (1 pad double per 8)
+    double *wsm = dsm;                                // [cells_y][bins][CX]
+    double *rows = dsm + cells_y * bins * CX;         // [2][bins][spad]
+    const int tiles_x = (nox + SC_COLS - 1) / SC_COLS;
+    const int tiles_y = (noy + SC_TY * SC_YG - 1) / (SC_TY * SC_YG);
+    int bid = blockIdx.x;
+    const int tx = bid % tiles_x;
+    bid /= tiles_x;
+    const int ty = bid % tiles_y;
+    const int f = bid / tiles_y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ix0 = tx * SC_COLS, iy0 = ty * SC_TY * SC_YG;
+    const int iyw = iy0 + warp * SC_TY;               // this warp's first window row
+    const int32_t *gf = grid + (int64_t)f * ncy * ncx * bins;
+    const double *df = den ? den + (int64_t)f * ncy * ncx : nullptr;
+
+    // weights, transposed to [cy][n][cx] for broadcast reads
+    for (int i = threadIdx.x; i < cells_y * CX * bins; i += blockDim.x) {
+        const int n = i % bins, cx = (i / bins) % CX, cy = i / (bins * CX);
+        wsm[(cy * bins + n) * CX + cx] = wts[i];
+    }
+    const int r_first = iy0, r_last = min(iy0 + SC_TY * SC_YG - 1, noy - 1) + (cells_y - 1) * K;
+    auto stage = [&](int r, int buf) {
+        double *dst = rows + buf * bins * spad;
+        const int32_t *src = gf + ((int64_t)r * ncx + ix0) * bins;
+        for (int i = threadIdx.x; i < span * bins; i += blockDim.x) {
+            const int c = i / bins, n = i % bins;
+            double v = 0.0;
+            if (ix0 + c < ncx && r < ncy) {
+                v = (double)src[i];
+                if (df) v = __ddiv_rn(v, df[(int64_t)r * ncx + ix0 + c]);
+            }
+            dst[n * spad + c + c / 8] = v;
+        }
+    };
+    double acc[SC_TY][SC_TX];
+#pragma unroll
+    for (int u = 0; u < SC_TY; ++u)
+#pragma unroll
+        for (int t = 0; t < SC_TX; ++t) acc[u][t] = 0.0;
+
+    stage(r_first, 0);
+    __syncthreads();
+    const int c0 = lane * SC_TX;  // this thread's first window column within the tile
+    for (int r = r_first; r <= r_last; ++r) {
+        const int buf = (r - r_first) & 1;
+        if (r < r_last) stage(r + 1, buf ^ 1);
+        const double *row = rows + buf * bins * spad;
+        int cyu[SC_TY];  // weight row each of this thread's window rows takes from grid row r
+#pragma unroll
+        for (int u = 0; u < SC_TY; ++u) {
+            const int d = r - (iyw + u);
+            cyu[u] = (d >= 0 && d % K == 0 && d / K < cells_y) ? d / K : -1;
+        }
+        for (int n = 0; n < bins; ++n) {
+            double gs[SC_TX + (CX - 1) * 2];
+            const double *rn = row + n * spad;
+            // cells this thread's windows touch: c0 .. c0 + SC_TX - 1 + (CX-1)*K
+#pragma unroll
+            for (int j = 0; j < SC_TX + (CX - 1) * 2; ++j) {
+                const int c = c0 + j;
+                gs[j] = (j < SC_TX + (CX - 1) * K && c < span) ? rn[c + c / 8] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < SC_TY; ++u) {
+                const int cy = cyu[u];
+                if (cy < 0) continue;
+                const double *wr = wsm + (cy * bins + n) * CX;
+                double w[CX];
+#pragma unroll
+                for (int cx = 0; cx < CX; ++cx) w[cx] = wr[cx];
+                if (K == 1) {
+#pragma unroll
+                    for (int t = 0; t < SC_TX; ++t)
+#pragma unroll
+                        for (int cx = 0; cx < CX; ++cx) acc[u][t] = fma(w[cx], gs[t + cx], acc[u][t]);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < SC_TX; ++t)
+#pragma unroll
+                        for (int cx = 0; cx < CX; ++cx) acc[u][t] = fma(w[cx], gs[t + 2 * cx], acc[u][t]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < SC_TY; ++u) {
+        const int iy = iyw + u;
+        if (iy >= noy) continue;
+#pragma unroll
+        for (int t = 0; t < SC_TX; ++t) {
+            const int ix = ix0 + c0 + t;
+            if (ix < nox) scores[((int64_t)f * noy + iy) * nox + ix] = acc[u][t] + bias;
+        }
+    }
+}
+
 // descriptor.py:107-124 + detector.py:148-150.  One thread per window.
 __global__ void k_window_features(const int32_t *__restrict__ grid, int ncy, int ncx, int bins,
                                   const int32_t *__restrict__ row_idx, int noy,
@@ -1187,6 +1304,30 @@ int hog_window_features(const int32_t *grid, int n, int ncy, int ncx, int bins,
         grid, ncy, ncx, bins, row_idx, noy, col_idx, nox, cells_x, cells_y, block, bstride, norm,
         eps_term, wts, bias, scores, desc, n);
     return check_launch("hog_window_features");
+}
+
+int hog_scores_lattice(const int32_t *grid, const double *den, int n, int ncy, int ncx, int bins,
+                       int noy, int nox, int cells_x, int cells_y, int k, const double *wts,
+                       double bias, double *scores, hog_stream_t stream) {
+    g_err.clear();
+    if (n < 1 || noy < 1 || nox < 1 || bins < 1 || !grid || !wts || !scores)
+        return fail(HOG_EINVAL, "bad arguments");
+    if (k != 1 && k != 2) return fail(HOG_EINVAL, "lattice step ratio must be 1 or 2, got %d", k);
+    if (cells_x != 8) return fail(HOG_EINVAL, "hog_scores_lattice is built for 8 cells across, got %d", cells_x);
+    if ((int64_t)(noy - 1) + (int64_t)(cells_y - 1) * k >= ncy || (int64_t)(nox - 1) + 7 * k >= ncx)
+        return fail(HOG_EINVAL, "window grid exceeds the cell lattice");
+    const int span = SC_COLS + 7 * k;
+    const size_t smem = sizeof(double) * ((size_t)cells_y * bins * 8 + 2 * (size_t)bins * (span + span / 8 + 1));
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(k_scores_lattice<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    const int64_t blocks = (int64_t)n * ((noy + SC_TY * SC_YG - 1) / (SC_TY * SC_YG)) *
+                           ((nox + SC_COLS - 1) / SC_COLS);
+    k_scores_lattice<8><<<(unsigned)blocks, 32 * SC_YG, smem, (cudaStream_t)stream>>>(
+        grid, den, ncy, ncx, bins, noy, nox, cells_y, k, wts, bias, scores);
+    return check_launch("hog_scores_lattice");
 }
 
 int hog_resize_bilinear(const uint8_t *src, int n, int c, int h, int w, int64_t sp, int64_t scs,

@@ -104,7 +104,13 @@ class HogPipeline:
             _native.call("hog_cell_norm", D.ptr(self.grid), self.n, self.ncx * self.ncy,
                          self.bins, _NORM_CODE[g.normalization], eps_term(g.normalization),
                          D.ptr(self.denom), s)
-        if self.scores is not None:
+        if self.scores is not None and self.fused and g.cells_x == 8:
+            _native.call("hog_scores_lattice", D.ptr(self.grid),
+                         D.ptr(self.denom) if self.denom is not None else None, self.n, self.ncy,
+                         self.ncx, self.bins, len(self.oys), len(self.oxs), g.cells_x, g.cells_y,
+                         self.cell // self.stride, D.ptr(self.w_dev), self.bias,
+                         D.ptr(self.scores), s)
+        elif self.scores is not None:
             _native.call("hog_window_features", D.ptr(self.grid), self.n, self.ncy, self.ncx,
                          self.bins, D.ptr(self.ri_dev), len(self.oys), D.ptr(self.ci_dev),
                          len(self.oxs), g.cells_x, g.cells_y, 1, 1, _NORM_CODE[g.normalization],

@@ -259,3 +259,23 @@ def test_native_library_is_the_one_loaded():
 
     lib = _native.load()
     assert os.path.samefile(lib._name, _native.LIB_PATH)
+
+
+@pytest.mark.parametrize("stride,norm", [(8, "none"), (4, "none"), (8, "l2"), (4, "l1")])
+def test_lattice_scores_vs_oracle(stride, norm):
+    # hog_scores_lattice (fused lattice path) against the oracle's per-window
+    # descriptor + dot (descriptor.py:107-124, detector.py:148-150)
+    cfg = synth.CONFIGS["c2"]
+    frames = synth.make_batch(cfg, 11, 2)[:, :, :200, :300].copy()
+    w = np.random.default_rng(stride * 10 + len(norm)).normal(0, 0.01, 1024)
+    p = H.HogPipeline(2, 1, 200, 300, 8, stride=stride, normalization=norm, weights=w, bias=0.25)
+    assert p.fused
+    p.upload(frames)
+    p.run()
+    torch.cuda.synchronize()
+    g = O.Geometry(64, 128, 8, 1, 1, 8, norm)
+    lut = O.build_lut(8)
+    for i in range(2):
+        planes = O.integral_stack(O.gradient_map(frames[i], lut), 8)
+        ref = O.scan_scores(planes, g, stride, w, 0.25)
+        np.testing.assert_allclose(p.scores[i].cpu().numpy(), ref, rtol=1e-9, atol=score_tol(w))
