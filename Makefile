@@ -1,20 +1,30 @@
 # Builds the sm_100a library (product) and the CPU oracle (test infrastructure).
+# `make -j` compiles the kernel translation units in parallel.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xptxas -v
+CSRC := paper_1703_06256_b200/csrc
+OBJDIR := build/obj
 LIB := paper_1703_06256_b200/libhogb200.so
-SRC := paper_1703_06256_b200/csrc/hog_kernels.cu
+UNITS := hog_abi k_bin k_planes_a k_planes_b k_planes_c k_planes_d k_window
+OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(UNITS)))
+HDRS := $(CSRC)/hog_common.cuh $(CSRC)/k_planes.cuh include/hogb200.h
 
 all: $(LIB) oracle
 
-$(LIB): $(SRC) include/hogb200.h
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) $(EXTRA) -c -o $@ $< 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+	cat $(OBJDIR)/*.ptxas.log > build_ptxas.log
 
 oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -f $(LIB) build_ptxas.log
+	rm -rf $(OBJDIR) $(LIB) build_ptxas.log
 	$(MAKE) -s -C oracle clean
 
 .PHONY: all oracle clean

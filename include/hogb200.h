@@ -47,6 +47,12 @@ typedef struct CUstream_st *hog_stream_t; /* == cudaStream_t */
 #define HOG_EINVAL 1
 #define HOG_ECUDA 2
 
+/* hog_pipeline stages (bitmask; 0 = all) */
+#define HOG_STAGE_BIN 1    /* gradient + LUT binning + per-band column counts */
+#define HOG_STAGE_SCAN 2   /* column counts above every band                  */
+#define HOG_STAGE_PLANES 4 /* integral planes (+ fused cell grid)             */
+#define HOG_STAGE_ALL 7
+
 /* Library version string, e.g. "hogb200 1.0 sm_100a". */
 const char *hog_version(void);
 
@@ -82,6 +88,9 @@ int hog_integral(const int8_t *binmap, int n, int h, int w, int64_t bm_pitch, in
  * `stride` up to ((ncx-1)*stride, (ncy-1)*stride)).  grid may be NULL (no
  * cell grid).  Requires stride % 4 == 0, cell % stride == 0, cell/stride <= 2
  * when grid != NULL; otherwise use hog_integral + hog_cell_grid.
+ * stages: HOG_STAGE_* bitmask (0 = all).  A caller may run the stages of one
+ * frame batch as separate calls on different streams (stage order per batch,
+ * same scratch), e.g. to bin batch j+1 while batch j writes its planes.
  * stage_events: NULL, or 4 cudaEvent_t recorded on `stream` before the
  * binning kernel, before the carry scans, before the plane kernel and after
  * it (lets a caller time each stage inside a larger timed region). */
@@ -91,7 +100,7 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w,
                  int8_t *binmap, int64_t bm_pitch, int64_t bm_fstride,
                  int32_t *planes, int64_t pl_pitch, int64_t pl_nstride, int64_t pl_fstride,
                  int cell, int stride, int ncx, int ncy, int32_t *grid,
-                 void *scratch, size_t scratch_bytes, void *const *stage_events,
+                 void *scratch, size_t scratch_bytes, int stages, void *const *stage_events,
                  hog_stream_t stream);
 
 /* descriptor.py:176-185 for an arbitrary (sorted) cell-origin set:

@@ -14,6 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HOGB200_LIB") or os.path.join(_HERE, "libhogb200.so")
 
 HOG_OK, HOG_EINVAL, HOG_ECUDA = 0, 1, 2
+STAGE_BIN, STAGE_SCAN, STAGE_PLANES, STAGE_ALL = 1, 2, 4, 7
 
 # (name, restype, argtypes) -- must match include/hogb200.h
 _P, _I, _L, _D, _SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
@@ -25,7 +26,7 @@ SIGNATURES = {
     "hog_scratch_bytes": (_SZ, [_I, _I, _I, _I, _I, _I]),
     "hog_integral": (_I, [_P, _I, _I, _I, _L, _L, _I, _P, _L, _L, _L, _P, _SZ, _P]),
     "hog_pipeline": (_I, [_P, _I, _I, _I, _I, _L, _L, _L, _P, _I, _P, _L, _L,
-                          _P, _L, _L, _L, _I, _I, _I, _I, _P, _P, _SZ, _P, _P]),
+                          _P, _L, _L, _L, _I, _I, _I, _I, _P, _P, _SZ, _I, _P, _P]),
     "hog_cell_grid": (_I, [_P, _I, _I, _I, _I, _L, _L, _L, _P, _I, _P, _I, _I, _P, _P]),
     "hog_cell_norm": (_I, [_P, _I, _I, _I, _I, _D, _P, _P]),
     "hog_window_features": (_I, [_P, _I, _I, _I, _I, _P, _I, _P, _I, _I, _I, _I, _I, _I, _D,

@@ -1,0 +1,332 @@
+// hog_abi.cu -- C ABI of libhogb200.so (include/hogb200.h): argument checks,
+// tile geometry, scratch carve-up, and kernel dispatch.  The kernels live in
+// k_bin.cu, k_planes_*.cu and k_window.cu.
+//
+// Reference: /root/reference/pkg/src/fasthog (pure Python + NumPy).  The hot
+// path is gradient.py:95-121 (LUT binning), integral.py:58-87 (per-bin
+// summed-area tables), descriptor.py:162-195 (cell histograms from 4 corner
+// reads) and detector.py:140-154 / 202-221 (scores, pyramid resize).
+//
+// Design (DESIGN.md has the roofline numbers):
+//   The integral planes (4*N_b bytes per pixel) are ~90% of the compulsory
+//   HBM traffic, so every plane element is written exactly once, with
+//   16-byte coalesced stores, by k_planes.  One warp owns a band of R plane
+//   rows of one frame and sweeps it strip by strip (4 columns per lane, 128
+//   columns per strip), walking down each strip: the row prefix is a warp
+//   scan of one-hot counts packed two bins per 32-bit word (16-bit lanes; a
+//   row prefix never exceeds the width), the column prefix lives in
+//   registers, and the row prefix left of the strip is handed from strip to
+//   strip through shared memory.  The only carry that crosses warps is the
+//   per-column count above the band: k_grad_bin counts bins per (band,
+//   column) while it bins the image, and k_scan_cols turns those counts into
+//   the column counts above every band.  When the scan lattice is regular,
+//   k_planes also emits the cell-histogram grid from the plane values it
+#include "hog_common.cuh"
+
+namespace hogb200 {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(HOG_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    return HOG_OK;
+}
+
+
+TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int cell, bool v8ok) {
+    TileGeom g{};
+    g.n = n; g.h = h; g.w = w; g.bins = bins;
+    g.NWB = (bins + 3) / 4;
+    g.NW = (bins + 1) / 2;
+    g.NWp = (int)round_up(g.NW, 4);
+    // 8 columns per lane only when every lattice column starts a lane chunk
+    g.VC = (v8ok && g.NW <= 5 && (!fused || stride % 8 == 0)) ? 8 : 4;
+    const int span = 32 * g.VC;
+    if (fused) {
+        int a = 8, b = stride;
+        while (b) { int r = a % b; a = b; b = r; }
+        const int l = 8 / a * stride;  // lcm(8, stride): strips start on lattice columns, 32-B aligned
+        g.Ws = ((span + stride - cell) / l) * l;
+        g.halo = cell - stride;
+    } else {
+        g.Ws = span;
+        g.halo = 0;
+    }
+    g.ns = (w + g.Ws - 1) / g.Ws;
+    g.NWARP = g.ns < 8 ? g.ns : 8;
+    g.nss = (g.ns + g.NWARP - 1) / g.NWARP;
+    g.nc1 = (w + CHUNK - 1) / CHUNK;
+    g.Wc = g.nc1 * CHUNK;
+    int R = 128;
+    const char *env = getenv("HOGB200_BAND_ROWS");
+    if (env && atoi(env) >= 8) {
+        R = atoi(env);
+    } else {
+        while (R > 16 && (int64_t)n * (h / R + 1) * g.NWARP < 148 * 32) R /= 2;
+    }
+    if (fused && R % stride != 0) R = (int)round_up(R, stride);
+    if (R > 240) R = 240;  // u8 column counts; packed strip-local sums stay < 2^16
+    g.R = R;
+    g.nb1 = (h + R - 1) / R;
+    g.nb2 = h / R + 1;
+    g.Lrows = R + g.halo;
+    return g;
+}
+
+size_t carve(const TileGeom &g, void *base, Scratch *sc) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += round_up((int64_t)bytes, 256);
+        return o;
+    };
+    size_t oC = take(sizeof(uint32_t) * (size_t)g.n * g.nb1 * g.Wc * g.NWB);
+    size_t oV = take(sizeof(uint32_t) * (size_t)g.n * g.nb2 * g.Wc * g.NWp);
+    if (sc && base) {
+        char *b = (char *)base;
+        sc->C = (uint32_t *)(b + oC);
+        sc->V = (uint32_t *)(b + oV);
+    }
+    return off;
+}
+
+
+int check_frames(int n, int h, int w) {
+    if (n < 1) return fail(HOG_EINVAL, "n must be >= 1, got %d", n);
+    if (h < 3 || w < 3) return fail(HOG_EINVAL, "need at least 3x3, got %dx%d", w, h);
+    if (h >= 65000 || w >= 65000) return fail(HOG_EINVAL, "frame %dx%d exceeds 65000 per side", w, h);
+    return HOG_OK;
+}
+
+int check_bins(int bins) {
+    if (bins < 2 || bins > 64) return fail(HOG_EINVAL, "bins must be in [2, 64], got %d", bins);
+    return HOG_OK;
+}
+
+int check_pitch4(const void *p, int64_t pitch, int w, const char *what) {
+    if (((uintptr_t)p & 3) != 0 || pitch % 4 != 0 || pitch < round_up(w, 4))
+        return fail(HOG_EINVAL, "%s: need 4-byte aligned base and pitch %% 4 == 0, pitch >= %lld (got %lld)",
+                    what, (long long)round_up(w, 4), (long long)pitch);
+    return HOG_OK;
+}
+
+PlaneOut make_po(int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, int w) {
+    PlaneOut po{pl, pp, pns, pfs, 0};
+    po.vec = (((uintptr_t)(pl + 1) & 31) == 0) && pp % 8 == 0 && pns % 8 == 0 && pfs % 8 == 0 &&
+             pp >= round_up(w, 8) + 8;
+    return po;
+}
+
+bool v8_ok(const PlaneOut &po, const int8_t *bm, int64_t bp, int64_t bfs) {
+    return po.vec && ((uintptr_t)bm & 7) == 0 && bp % 8 == 0 && bfs % 8 == 0;
+}
+
+int integral_impl(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w, int bins,
+                  int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, void *scratch, size_t sbytes,
+                  cudaStream_t st) {
+    PlaneOut po = make_po(pl, pp, pns, pfs, w);
+    if (bins > MAX_FUSED_BINS) {
+        launch_generic_integral(bm, bp, bfs, po, n, h, w, bins, st);
+        return check_launch("integral (generic)");
+    }
+    TileGeom g = make_geom(n, h, w, bins, false, 0, 0, v8_ok(po, bm, bp, bfs));
+    Scratch sc{};
+    size_t need = carve(g, nullptr, nullptr);
+    if (scratch == nullptr || sbytes < need)
+        return fail(HOG_EINVAL, "scratch too small: need %zu bytes, got %zu", need, sbytes);
+    carve(g, scratch, &sc);
+    GridOut go{nullptr, 4, 4, 1, 1};
+    launch_counts_from_bm(g.NW, bm, bp, bfs, g, sc, st);
+    launch_scan(g.NW, g, sc, st);
+    launch_planes(g.NW, 0, bm, bp, bfs, po, go, g, sc, st);
+    return check_launch("hog_integral");
+}
+
+}  // namespace hogb200
+
+using namespace hogb200;
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+const char *hog_version(void) { return "hogb200 1.2 sm_100a"; }
+
+const char *hog_last_error(void) { return g_err.c_str(); }
+
+int64_t hog_plane_pitch(int w) { return round_up((int64_t)w, 8) + 8; }
+
+int hog_grad_bin(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int64_t ics,
+                 int64_t ifs, const uint8_t *lut, int bins, int8_t *bm, int64_t bp, int64_t bfs,
+                 hog_stream_t stream) {
+    g_err.clear();
+    int e;
+    if ((e = check_frames(n, h, w)) || (e = check_bins(bins))) return e;
+    if (c != 1 && c != 3) return fail(HOG_EINVAL, "channels must be 1 or 3, got %d", c);
+    if ((e = check_pitch4(img, ip, w, "image")) || (e = check_pitch4(bm, bp, w, "binmap"))) return e;
+    if (!img || !lut || !bm) return fail(HOG_EINVAL, "null buffer");
+    TileGeom g = make_geom(n, h, w, bins, false, 0, 0, false);
+    Scratch sc{};
+    launch_grad_bin(1, c, false, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, (cudaStream_t)stream);
+    return check_launch("hog_grad_bin");
+}
+
+size_t hog_scratch_bytes(int n, int h, int w, int bins, int stride, int cell) {
+    if (n < 1 || h < 1 || w < 1 || bins < 1) return 0;
+    bool fused = stride > 0 && cell > 0;
+    size_t m = 0;
+    for (int v8 = 0; v8 < 2; ++v8) {
+        size_t a = carve(make_geom(n, h, w, bins, fused, stride, cell, v8), nullptr, nullptr);
+        size_t b = carve(make_geom(n, h, w, bins, false, 0, 0, v8), nullptr, nullptr);
+        m = a > m ? a : m;
+        m = b > m ? b : m;
+    }
+    return m;
+}
+
+int hog_integral(const int8_t *bm, int n, int h, int w, int64_t bp, int64_t bfs, int bins,
+                 int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, void *scratch,
+                 size_t sbytes, hog_stream_t stream) {
+    g_err.clear();
+    int e;
+    if ((e = check_frames(n, h, w)) || (e = check_bins(bins))) return e;
+    if ((e = check_pitch4(bm, bp, w, "binmap"))) return e;
+    if (pp < (int64_t)w + 1) return fail(HOG_EINVAL, "plane pitch %lld < w+1", (long long)pp);
+    if (!bm || !pl) return fail(HOG_EINVAL, "null buffer");
+    return integral_impl(bm, bp, bfs, n, h, w, bins, pl, pp, pns, pfs, scratch, sbytes,
+                         (cudaStream_t)stream);
+}
+
+int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int64_t ics,
+                 int64_t ifs, const uint8_t *lut, int bins, int8_t *bm, int64_t bp, int64_t bfs,
+                 int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, int cell, int stride, int ncx,
+                 int ncy, int32_t *grid, void *scratch, size_t sbytes, int stages,
+                 void *const *stage_events, hog_stream_t stream) {
+    g_err.clear();
+    if (stages == 0) stages = HOG_STAGE_ALL;
+    int e;
+    if ((e = check_frames(n, h, w)) || (e = check_bins(bins))) return e;
+    if (c != 1 && c != 3) return fail(HOG_EINVAL, "channels must be 1 or 3, got %d", c);
+    if ((e = check_pitch4(img, ip, w, "image")) || (e = check_pitch4(bm, bp, w, "binmap"))) return e;
+    if (pp < (int64_t)w + 1) return fail(HOG_EINVAL, "plane pitch %lld < w+1", (long long)pp);
+    if (!img || !lut || !bm || !pl) return fail(HOG_EINVAL, "null buffer");
+    if (bins > MAX_FUSED_BINS)
+        return fail(HOG_EINVAL, "fused pipeline supports bins <= %d (got %d); use hog_grad_bin + "
+                    "hog_integral + hog_cell_grid", MAX_FUSED_BINS, bins);
+    int kr = 0;
+    if (grid) {
+        if (stride <= 0 || stride % 4 != 0 || cell % stride != 0 || cell / stride > 2 || cell % 4 != 0)
+            return fail(HOG_EINVAL, "fused grid needs stride %% 4 == 0, cell %% stride == 0, "
+                        "cell/stride <= 2 (stride %d, cell %d)", stride, cell);
+        if (ncx < 1 || ncy < 1 || (int64_t)(ncx - 1) * stride + cell > w ||
+            (int64_t)(ncy - 1) * stride + cell > h)
+            return fail(HOG_EINVAL, "cell lattice %dx%d (step %d, cell %d) exceeds %dx%d", ncx, ncy,
+                        stride, cell, w, h);
+        kr = cell / stride;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    PlaneOut po = make_po(pl, pp, pns, pfs, w);
+    TileGeom g = make_geom(n, h, w, bins, kr > 0, stride, cell, v8_ok(po, bm, bp, bfs));
+    Scratch sc{};
+    size_t need = carve(g, nullptr, nullptr);
+    if (scratch == nullptr || sbytes < need)
+        return fail(HOG_EINVAL, "scratch too small: need %zu bytes, got %zu", need, sbytes);
+    carve(g, scratch, &sc);
+    GridOut go{grid, kr ? stride : 4, kr ? cell : 4, kr ? ncx : 1, kr ? ncy : 1};
+    auto mark = [&](int i) {
+        if (stage_events && stage_events[i]) cudaEventRecord((cudaEvent_t)stage_events[i], st);
+    };
+    mark(0);
+    if (stages & HOG_STAGE_BIN)
+        launch_grad_bin(g.NWB, c, true, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st);
+    mark(1);
+    if (stages & HOG_STAGE_SCAN) launch_scan(g.NW, g, sc, st);
+    mark(2);
+    if (stages & HOG_STAGE_PLANES) launch_planes(g.NW, kr, bm, bp, bfs, po, go, g, sc, st);
+    mark(3);
+    return check_launch("hog_pipeline");
+}
+
+int hog_cell_grid(const int32_t *pl, int n, int h, int w, int bins, int64_t pp, int64_t pns,
+                  int64_t pfs, const int32_t *cxs, int ncx, const int32_t *cys, int ncy, int cell,
+                  int32_t *grid, hog_stream_t stream) {
+    g_err.clear();
+    int e;
+    if ((e = check_frames(n, h, w)) || (e = check_bins(bins))) return e;
+    if (ncx < 1 || ncy < 1 || cell < 1) return fail(HOG_EINVAL, "empty cell lattice");
+    if (!pl || !cxs || !cys || !grid) return fail(HOG_EINVAL, "null buffer");
+    launch_cell_grid(pl, pp, pns, pfs, n, bins, cxs, ncx, cys, ncy, cell, grid, (cudaStream_t)stream);
+    return check_launch("hog_cell_grid");
+}
+
+int hog_cell_norm(const int32_t *grid, int n, int ncells, int bins, int norm, double eps_term,
+                  double *den, hog_stream_t stream) {
+    g_err.clear();
+    if (norm != 1 && norm != 2) return fail(HOG_EINVAL, "norm must be 1 (l1) or 2 (l2)");
+    if (n < 1 || ncells < 1 || bins < 1 || !grid || !den) return fail(HOG_EINVAL, "bad arguments");
+    const int64_t tot = (int64_t)n * ncells;
+    launch_cell_norm(grid, tot, bins, norm, eps_term, den, (cudaStream_t)stream);
+    return check_launch("hog_cell_norm");
+}
+
+int hog_window_features(const int32_t *grid, int n, int ncy, int ncx, int bins,
+                        const int32_t *row_idx, int noy, const int32_t *col_idx, int nox,
+                        int cells_x, int cells_y, int block, int bstride, int norm,
+                        double eps_term, const double *wts, double bias, double *scores,
+                        double *desc, hog_stream_t stream) {
+    g_err.clear();
+    if (n < 1 || noy < 1 || nox < 1 || bins < 1 || !grid || !row_idx || !col_idx)
+        return fail(HOG_EINVAL, "bad arguments");
+    if (block < 1 || block > cells_x || block > cells_y || bstride < 1)
+        return fail(HOG_EINVAL, "block %d / stride %d do not fit %dx%d cells", block, bstride,
+                    cells_x, cells_y);
+    if (norm < 0 || norm > 2) return fail(HOG_EINVAL, "norm must be 0, 1 or 2");
+    if (scores && !wts) return fail(HOG_EINVAL, "scores need weights");
+    const int64_t tot = (int64_t)n * noy * nox;
+    launch_window_features(grid, n, ncy, ncx, bins, row_idx, noy, col_idx, nox, cells_x, cells_y,
+                           block, bstride, norm, eps_term, wts, bias, scores, desc,
+                           (cudaStream_t)stream);
+    return check_launch("hog_window_features");
+}
+
+int hog_scores_lattice(const int32_t *grid, const double *den, int n, int ncy, int ncx, int bins,
+                       int noy, int nox, int cells_x, int cells_y, int k, const double *wts,
+                       double bias, double *scores, hog_stream_t stream) {
+    g_err.clear();
+    if (n < 1 || noy < 1 || nox < 1 || bins < 1 || !grid || !wts || !scores)
+        return fail(HOG_EINVAL, "bad arguments");
+    if (k != 1 && k != 2) return fail(HOG_EINVAL, "lattice step ratio must be 1 or 2, got %d", k);
+    if (cells_x != 8) return fail(HOG_EINVAL, "hog_scores_lattice is built for 8 cells across, got %d", cells_x);
+    if ((int64_t)(noy - 1) + (int64_t)(cells_y - 1) * k >= ncy || (int64_t)(nox - 1) + 7 * k >= ncx)
+        return fail(HOG_EINVAL, "window grid exceeds the cell lattice");
+    launch_scores_lattice(grid, den, n, ncy, ncx, bins, noy, nox, cells_y, k, wts, bias, scores,
+                          (cudaStream_t)stream);
+    return check_launch("hog_scores_lattice");
+}
+
+int hog_resize_bilinear(const uint8_t *src, int n, int c, int h, int w, int64_t sp, int64_t scs,
+                        int64_t sfs, int nh, int nw, double ry, double rx, uint8_t *dst,
+                        int64_t dp, int64_t dcs, int64_t dfs, hog_stream_t stream) {
+    g_err.clear();
+    if (n < 1 || c < 1 || h < 1 || w < 1 || nh < 1 || nw < 1 || !src || !dst)
+        return fail(HOG_EINVAL, "bad arguments");
+    const int64_t tot = (int64_t)n * c * nh * nw;
+    launch_resize(src, n, c, h, w, sp, scs, sfs, nh, nw, ry, rx, dst, dp, dcs, dfs,
+                  (cudaStream_t)stream);
+    return check_launch("hog_resize_bilinear");
+}
+
+}  // extern "C"

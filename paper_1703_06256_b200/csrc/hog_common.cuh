@@ -1,0 +1,212 @@
+// hog_common.cuh -- types, device helpers and launcher declarations shared by
+// the libhogb200 translation units (k_bin.cu, k_planes_*.cu, k_window.cu,
+// hog_abi.cu).  See hog_abi.cu for the design overview.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/hogb200.h"
+
+namespace hogb200 {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int LUT_SIDE = 511;
+constexpr int K_THREADS = 128;      // 4 independent warps per CTA
+constexpr int MAX_FUSED_BINS = 18;  // NW <= 9 packed words
+constexpr int CHUNK = 128;          // k_grad_bin columns per warp (32 lanes x 4)
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// ---------------------------------------------------------------------------
+// Geometry shared by k_grad_bin / k_bin_counts / k_scan_cols / k_planes.
+struct TileGeom {
+    int n, h, w, bins;
+    int R;      // rows per band (multiple of the lattice step when the grid is fused)
+    int Ws;     // plane columns per k_planes strip (<= 128, multiple of 8)
+    int ns;     // strips per frame
+    int nb1;    // pixel bands: ceil(h / R)         (k_grad_bin tiles)
+    int nb2;    // plane bands: h / R + 1            (k_planes tiles; plane rows 0..h)
+    int nc1;    // 128-column chunks: ceil(w / 128)  (k_grad_bin tiles)
+    int Wc;     // nc1 * 128: padded width of the per-column scratch arrays
+    int NWB;    // u8x4 words per column count   = ceil(bins / 4)
+    int NW;     // u16x2 words per row count     = ceil(bins / 2)
+    int NWp;    // NW padded to a multiple of 4 (16-byte V rows)
+    int halo;   // extra rows a band computes for straddling cells (cell - step)
+    int Lrows;  // rows of row-carry state (R + halo)
+    int VC;     // plane columns per lane in k_planes (8: 256-bit stores, 4: 128-bit)
+    int NWARP;  // warps (strips) per k_planes CTA
+    int nss;    // super-strips: ceil(ns / NWARP)
+};
+
+// Scratch arrays (device), carved from the caller's scratch buffer.
+struct Scratch {
+    uint32_t *C;  // [n][nb1][Wc][NWB]  bin counts per (pixel band, column), u8x4
+    uint32_t *V;  // [n][nb2][Wc][NWp]  counts above each plane band, u16x2
+};
+
+
+// ---------------------------------------------------------------------------
+// K2: integral planes (+ fused cell grid).  integral.py:58-87,
+// descriptor.py:176-185.  KR = cell / lattice step (0: no grid); VC = plane
+// columns per lane (8: one 256-bit store per plane row, 4: 128-bit).
+//
+// CTA = (frame f, band b): plane rows [Y0, Y0+R) (+ `halo` rows computed for
+// cells straddling the band).  Its NWARP warps own adjacent column strips and
+// walk the band's rows together, so every plane row leaves the SM as one
+// contiguous burst (HBM write efficiency: tools/probe_store.cu).  In a strip,
+// lane L holds P(Y, X) for its VC columns and every bin in registers (acc).
+// Row Y -> Y+1 adds the row prefix R(Y, X) = Lc(Y) + (warp-exclusive count) +
+// (lane-local count); Lc(Y), the count left of the strip, is the sum of the
+// strip totals of the warps to the left, exchanged through shared memory once
+// per group of G rows (phase A: warp scans + strip totals, barrier, phase B:
+// accumulate + store).  Frames wider than NWARP strips are swept in
+// super-strips, carrying Lc through shared memory.  Lattice row Yl:
+// Hd(Yl, xi) = P(Yl, xi + cell) - P(Yl, xi) by shuffles, and the cell with
+// top-left (Yl - cell, xi) is Hd(Yl) - Hd(Yl - cell) (per-lane ring in smem).
+
+struct PlaneOut {
+    int32_t *pl;
+    int64_t pp, pns, pfs;
+    int vec;  // 32-B aligned rows: vector stores + full-sector padding writes
+};
+
+struct GridOut {
+    int32_t *grid;
+    int s, cell, ncx, ncy;
+};
+
+constexpr int K2_G = 4;  // rows per phase-A/phase-B group
+
+// shared-memory carve-up of one k_planes CTA (32-bit words, every array 16-B aligned)
+struct K2Smem {
+    int rowtot, Lsup, vtot, Tsup, ptop, ring, total;
+};
+
+__host__ __device__ inline int k2_r4(int v) { return (v + 3) & ~3; }
+
+__host__ __device__ inline K2Smem k2_smem(const TileGeom &g, int kr) {
+    const int NB = 2 * g.NW;
+    K2Smem m;
+    m.rowtot = 0;                                                // [2][G][NWARP][NWp]
+    m.Lsup = m.rowtot + k2_r4(2 * K2_G * g.NWARP * g.NWp);       // [2][Lrows][NWp]
+    m.vtot = m.Lsup + k2_r4(2 * g.Lrows * g.NWp);                // [NWARP][NB]
+    m.Tsup = m.vtot + k2_r4(g.NWARP * NB);                       // [2][NB]
+    m.ptop = m.Tsup + k2_r4(2 * NB);                             // [NWARP][NB][32][VC]
+    m.ring = m.ptop + k2_r4(g.NWARP * NB * 32 * g.VC);           // [NWARP][KR][NB][32]
+    m.total = m.ring + k2_r4(g.NWARP * kr * NB * 32);
+    return m;
+}
+
+__host__ __device__ inline int k2_smem_words(const TileGeom &g, int kr) { return k2_smem(g, kr).total; }
+
+
+// ---------------------------------------------------------------------------
+// Device helpers
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t t = __shfl_up_sync(FULL, v, d);
+        if (lane >= d) v += t;
+    }
+    return v;
+}
+
+__device__ __forceinline__ uint32_t byte_of(uint32_t v, int k) { return (v >> (8 * k)) & 0xffu; }
+
+// u8x4 word -> u16x2 word holding bytes (2h, 2h+1)
+__device__ __forceinline__ uint32_t widen_half(uint32_t v, int h) {
+    return h == 0 ? __byte_perm(v, 0u, 0x4140) : __byte_perm(v, 0u, 0x4342);
+}
+
+__device__ __forceinline__ uint32_t half16(uint32_t v, int h) {
+    return h == 0 ? (v & 0xffffu) : (v >> 16);
+}
+
+__device__ __forceinline__ int64_t warp_id() {
+    return (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+}
+
+// Per-lane column counts of 4 pixel bins (bytes of `bins4`, 0xFF = none):
+// cc[k][w] holds bins 4w..4w+3 of column k as u8x4.
+template <int NWB>
+__device__ __forceinline__ void count_cols(uint32_t bins4, uint32_t (&cc)[4][NWB]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t v = byte_of(bins4, k);
+        const uint32_t q = v >> 2, one = 1u << ((v & 3u) << 3);
+#pragma unroll
+        for (int w = 0; w < NWB; ++w)
+            if (q == (uint32_t)w) cc[k][w] += one;
+    }
+}
+
+template <int NWB>
+__device__ __forceinline__ void store_cols(const TileGeom &g, const Scratch &sc, int f, int b,
+                                           int x, uint32_t (&cc)[4][NWB]) {
+    uint32_t *cp = sc.C + (((int64_t)f * g.nb1 + b) * g.Wc + x) * NWB;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int w = 0; w < NWB; ++w) cp[k * NWB + w] = cc[k][w];
+}
+
+
+inline unsigned blocks_for_warps(int64_t warps) {
+    return (unsigned)((warps + (K_THREADS / 32) - 1) / (K_THREADS / 32));
+}
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// ---- launchers (defined in the kernel translation units) -------------------
+// k_bin.cu
+void launch_grad_bin(int nwb, int c, bool counts, const uint8_t *img, int64_t ip, int64_t ics,
+                     int64_t ifs, const uint8_t *lut, int8_t *bm, int64_t bp, int64_t bfs,
+                     const TileGeom &g, const Scratch &sc, cudaStream_t st);
+void launch_counts_from_bm(int nw, const int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g,
+                           const Scratch &sc, cudaStream_t st);
+void launch_scan(int nw, const TileGeom &g, const Scratch &sc, cudaStream_t st);
+// k_planes_*.cu
+void launch_planes_a(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                     const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st);
+void launch_planes_b(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                     const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st);
+void launch_planes_c(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                     const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st);
+void launch_planes_d(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                     const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st);
+inline void launch_planes(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs,
+                          const PlaneOut &po, const GridOut &go, const TileGeom &g,
+                          const Scratch &sc, cudaStream_t st) {
+    if (nw <= 3) launch_planes_a(nw, kr, bm, bp, bfs, po, go, g, sc, st);
+    else if (nw <= 5) launch_planes_b(nw, kr, bm, bp, bfs, po, go, g, sc, st);
+    else if (nw <= 7) launch_planes_c(nw, kr, bm, bp, bfs, po, go, g, sc, st);
+    else launch_planes_d(nw, kr, bm, bp, bfs, po, go, g, sc, st);
+}
+// k_window.cu
+void launch_generic_integral(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po, int n,
+                             int h, int w, int bins, cudaStream_t st);
+void launch_cell_grid(const int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, int n, int bins,
+                      const int32_t *cxs, int ncx, const int32_t *cys, int ncy, int cell,
+                      int32_t *grid, cudaStream_t st);
+void launch_cell_norm(const int32_t *grid, int64_t ncells_total, int bins, int norm,
+                      double eps_term, double *den, cudaStream_t st);
+void launch_window_features(const int32_t *grid, int n, int ncy, int ncx, int bins,
+                            const int32_t *row_idx, int noy, const int32_t *col_idx, int nox,
+                            int cells_x, int cells_y, int block, int bstride, int norm,
+                            double eps_term, const double *wts, double bias, double *scores,
+                            double *desc, cudaStream_t st);
+void launch_scores_lattice(const int32_t *grid, const double *den, int n, int ncy, int ncx,
+                           int bins, int noy, int nox, int cells_y, int k, const double *wts,
+                           double bias, double *scores, cudaStream_t st);
+void launch_resize(const uint8_t *src, int n, int c, int h, int w, int64_t sp, int64_t scs,
+                   int64_t sfs, int nh, int nw, double ry, double rx, uint8_t *dst, int64_t dp,
+                   int64_t dcs, int64_t dfs, cudaStream_t st);
+
+}  // namespace hogb200

@@ -1,0 +1,234 @@
+// k_bin.cu -- K1: gradient + LUT binning with per-(band, column) bin counts,
+// and the carry scan that turns the counts into column counts above every
+// band.  gradient.py:95-121; integral.py:58-87 (the carries of the scan).
+#include "hog_common.cuh"
+
+namespace hogb200 {
+
+// ---------------------------------------------------------------------------
+// K1: gradient + LUT binning (gradient.py:95-121), optionally counting bins
+// per (band, column) for k_scan_cols.  One warp = R rows x 128 columns of
+// one frame; lane L owns pixel columns x0+4L .. x0+4L+3 and slides a
+// three-row window down the band, two rows of loads in flight; left/right
+// neighbours come from the adjacent lanes by shuffle.
+
+template <int CH, int NWB, bool COUNTS>
+__global__ void __launch_bounds__(K_THREADS)
+k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs,
+           const uint8_t *__restrict__ lut, int8_t *__restrict__ bm, int64_t bp, int64_t bfs,
+           TileGeom g, Scratch sc) {
+    const int64_t wid = warp_id();
+    if (wid >= (int64_t)g.n * g.nb1 * g.nc1) return;
+    const int chunk = (int)(wid % g.nc1);
+    const int b = (int)((wid / g.nc1) % g.nb1);
+    const int f = (int)(wid / ((int64_t)g.nc1 * g.nb1));
+    const int lane = threadIdx.x & 31;
+    const int x = chunk * CHUNK + 4 * lane;
+    const bool inx = x < g.w;
+    const int y0 = b * g.R, y1 = min(y0 + g.R, g.h);
+    // lanes past the frame read (and discard) the last word of the row
+    const int xl = inx ? x : ((g.w - 1) & ~3);
+    const uint8_t *col = img + (int64_t)f * ifs + xl;
+    const uint8_t *lut0 = lut + (255 * LUT_SIDE + 255);  // lut0[dx*511 + dy]
+
+    // bytes of this lane's 4 columns that are interior pixels (1 <= x <= w-2)
+    uint32_t valid = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (x + k >= 1 && x + k <= g.w - 2) valid |= 0xffu << (8 * k);
+    // neighbour byte outside the lane's word: left of lane 0, right of lane 31
+    const int eoff = lane == 0 ? -1 : 4;
+    const bool has_edge = (lane == 0 && x >= 1) || (lane == 31 && x + 4 < g.w);
+    auto rowp = [&](int y) { return col + (int64_t)min(max(y, 0), g.h - 1) * ip; };
+
+    // rows y-1 (r0), y (r1), y+1 (r2); e1/e2: edge bytes of rows y, y+1
+    uint32_t r0[CH], r1[CH], r2[CH], e1[CH], e2[CH];
+    {
+        const uint8_t *pa = rowp(y0 - 1), *pb = rowp(y0), *pc = rowp(y0 + 1);
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+            r0[ch] = __ldg(reinterpret_cast<const uint32_t *>(pa + ch * ics));
+            r1[ch] = __ldg(reinterpret_cast<const uint32_t *>(pb + ch * ics));
+            r2[ch] = __ldg(reinterpret_cast<const uint32_t *>(pc + ch * ics));
+            e1[ch] = has_edge ? (uint32_t)__ldg(pb + ch * ics + eoff) : 0u;
+            e2[ch] = has_edge ? (uint32_t)__ldg(pc + ch * ics + eoff) : 0u;
+        }
+    }
+    uint32_t cc[4][NWB];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int w = 0; w < NWB; ++w) cc[k][w] = 0;
+    int8_t *bout = bm + (int64_t)f * bfs + (int64_t)y0 * bp + x;
+
+    for (int y = y0; y < y1; ++y) {
+        // row y+2 in flight while row y is binned
+        uint32_t r3[CH], e3[CH];
+        const uint8_t *pd = rowp(y + 2);
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+            r3[ch] = __ldg(reinterpret_cast<const uint32_t *>(pd + ch * ics));
+            e3[ch] = has_edge ? (uint32_t)__ldg(pd + ch * ics + eoff) : 0u;
+        }
+        uint32_t bins4 = 0xffffffffu;
+        if (y > 0 && y < g.h - 1) {
+            int bdx[4], bdy[4], bmag[4];
+#pragma unroll
+            for (int ch = 0; ch < CH; ++ch) {
+                const uint32_t prev = __shfl_up_sync(FULL, r1[ch], 1);
+                const uint32_t next = __shfl_down_sync(FULL, r1[ch], 1);
+                // Lw: bytes at x-1..x+2, Rw: bytes at x+1..x+4
+                const uint32_t Lw = __byte_perm(lane == 0 ? e1[ch] : prev >> 24, r1[ch], 0x6540);
+                const uint32_t Rw = __byte_perm(r1[ch], lane == 31 ? e1[ch] : next, 0x4321);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int dx = (int)byte_of(Rw, k) - (int)byte_of(Lw, k);
+                    const int dy = (int)byte_of(r2[ch], k) - (int)byte_of(r0[ch], k);
+                    if (CH == 1) {
+                        bdx[k] = dx, bdy[k] = dy;
+                    } else {
+                        // gradient.py:113-117: largest dx^2+dy^2 wins, first channel on ties
+                        const int mag = dx * dx + dy * dy;
+                        if (ch == 0 || mag > bmag[k]) bdx[k] = dx, bdy[k] = dy, bmag[k] = mag;
+                    }
+                }
+            }
+            uint32_t v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = __ldg(lut0 + (bdx[k] * LUT_SIDE + bdy[k]));
+            bins4 = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+            bins4 = (bins4 & valid) | ~valid;
+        }
+        if (inx) *reinterpret_cast<uint32_t *>(bout) = bins4;
+        bout += bp;
+        if (COUNTS) count_cols<NWB>(bins4, cc);
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+            r0[ch] = r1[ch];
+            r1[ch] = r2[ch];
+            r2[ch] = r3[ch];
+            e1[ch] = e2[ch];
+            e2[ch] = e3[ch];
+        }
+    }
+    if (COUNTS) store_cols<NWB>(g, sc, f, b, x, cc);
+}
+
+// K1': the same per-(band, column) counts from an existing bin map (hog_integral).
+template <int NWB>
+__global__ void __launch_bounds__(K_THREADS)
+k_bin_counts(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, TileGeom g, Scratch sc) {
+    const int64_t wid = warp_id();
+    if (wid >= (int64_t)g.n * g.nb1 * g.nc1) return;
+    const int chunk = (int)(wid % g.nc1);
+    const int b = (int)((wid / g.nc1) % g.nb1);
+    const int f = (int)(wid / ((int64_t)g.nc1 * g.nb1));
+    const int lane = threadIdx.x & 31;
+    const int x = chunk * CHUNK + 4 * lane;
+    const int y0 = b * g.R, y1 = min(y0 + g.R, g.h);
+    const int8_t *bmf = bm + (int64_t)f * bfs;
+    uint32_t mask = 0;  // bytes past w count nowhere
+    if (x + 4 > g.w) mask = x >= g.w ? 0xffffffffu : 0xffffffffu << (8 * (g.w - x));
+    uint32_t cc[4][NWB];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int w = 0; w < NWB; ++w) cc[k][w] = 0;
+    for (int y = y0; y < y1; ++y) {
+        uint32_t v = 0xffffffffu;
+        if (x < g.w) v = __ldg(reinterpret_cast<const uint32_t *>(bmf + (int64_t)y * bp + x)) | mask;
+        count_cols<NWB>(v, cc);
+    }
+    store_cols<NWB>(g, sc, f, b, x, cc);
+}
+
+// V[f][b][x] = sum over pixel bands b' < b of C[f][b'][x]: column counts of
+// plane rows [0, b*R), u16x2 packed (<= h < 65536).
+template <int NWB, int NW>
+__global__ void k_scan_cols(TileGeom g, Scratch sc) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)g.n * g.Wc) return;
+    const int f = (int)(i / g.Wc), x = (int)(i % g.Wc);
+    uint32_t run[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) run[w] = 0;
+    for (int b = 0; b < g.nb2; ++b) {
+        uint32_t *vp = sc.V + (((int64_t)f * g.nb2 + b) * g.Wc + x) * g.NWp;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) vp[w] = run[w];
+        for (int w = NW; w < g.NWp; ++w) vp[w] = 0;
+        if (b < g.nb1) {
+            const uint32_t *cp = sc.C + (((int64_t)f * g.nb1 + b) * g.Wc + x) * NWB;
+            uint32_t c8[NWB];
+#pragma unroll
+            for (int w = 0; w < NWB; ++w) c8[w] = cp[w];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) run[w] += widen_half(c8[w >> 1], w & 1);
+        }
+    }
+}
+
+template <int NWB>
+void grad_bin_t(int c, bool counts, const uint8_t *img, int64_t ip, int64_t ics, int64_t ifs,
+                const uint8_t *lut, int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g,
+                const Scratch &sc, cudaStream_t st) {
+    const unsigned nb = blocks_for_warps((int64_t)g.n * g.nb1 * g.nc1);
+#define LAUNCH(CHv, CNT) \
+    k_grad_bin<CHv, NWB, CNT><<<nb, K_THREADS, 0, st>>>(img, ip, ics, ifs, lut, bm, bp, bfs, g, sc)
+    if (c == 1) {
+        if (counts) LAUNCH(1, true); else LAUNCH(1, false);
+    } else {
+        if (counts) LAUNCH(3, true); else LAUNCH(3, false);
+    }
+#undef LAUNCH
+}
+
+void launch_grad_bin(int nwb, int c, bool counts, const uint8_t *img, int64_t ip, int64_t ics,
+                     int64_t ifs, const uint8_t *lut, int8_t *bm, int64_t bp, int64_t bfs,
+                     const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+    switch (nwb) {
+        case 1: grad_bin_t<1>(c, counts, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st); break;
+        case 2: grad_bin_t<2>(c, counts, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st); break;
+        case 3: grad_bin_t<3>(c, counts, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st); break;
+        case 4: grad_bin_t<4>(c, counts, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st); break;
+        default: grad_bin_t<5>(c, counts, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st); break;
+    }
+}
+
+template <int NW>
+void scan_t(const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+    constexpr int NWB = (2 * NW + 3) / 4;
+    k_scan_cols<NWB, NW><<<blocks_for((int64_t)g.n * g.Wc, 256), 256, 0, st>>>(g, sc);
+}
+
+template <int NW>
+void counts_t(const int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g, const Scratch &sc,
+              cudaStream_t st) {
+    constexpr int NWB = (2 * NW + 3) / 4;
+    k_bin_counts<NWB><<<blocks_for_warps((int64_t)g.n * g.nb1 * g.nc1), K_THREADS, 0, st>>>(
+        bm, bp, bfs, g, sc);
+}
+
+#define HOG_NW_DISPATCH(nw, FN, ...)       \
+    switch (nw) {                          \
+        case 1: FN<1>(__VA_ARGS__); break; \
+        case 2: FN<2>(__VA_ARGS__); break; \
+        case 3: FN<3>(__VA_ARGS__); break; \
+        case 4: FN<4>(__VA_ARGS__); break; \
+        case 5: FN<5>(__VA_ARGS__); break; \
+        case 6: FN<6>(__VA_ARGS__); break; \
+        case 7: FN<7>(__VA_ARGS__); break; \
+        case 8: FN<8>(__VA_ARGS__); break; \
+        default: FN<9>(__VA_ARGS__); break; \
+    }
+
+void launch_scan(int nw, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+    HOG_NW_DISPATCH(nw, scan_t, g, sc, st)
+}
+
+void launch_counts_from_bm(int nw, const int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g,
+                           const Scratch &sc, cudaStream_t st) {
+    HOG_NW_DISPATCH(nw, counts_t, bm, bp, bfs, g, sc, st)
+}
+
+}  // namespace hogb200

@@ -1,0 +1,379 @@
+// k_planes.cuh -- K2: the single-write integral-plane kernel (+ fused cell
+// grid).  Included by k_planes_{a,b,c,d}.cu, each instantiating a range of
+// packed-word counts NW (bins = 2*NW or 2*NW-1) to keep builds parallel.
+#pragma once
+#include "hog_common.cuh"
+
+namespace hogb200 {
+
+template <int VC>
+__device__ __forceinline__ void store_chunk(int32_t *p, const uint32_t (&v)[VC], bool vec, int valid) {
+    if (vec) {
+        if constexpr (VC == 8) {
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]),
+                         "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                         : "memory");
+        } else {
+            *reinterpret_cast<int4 *>(p) = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < VC; ++k)
+            if (k < valid) p[k] = (int)v[k];
+    }
+}
+
+template <int VC>
+struct BmWord;
+template <>
+struct BmWord<4> {
+    uint32_t w;
+    __device__ __forceinline__ uint32_t byte(int k) const { return byte_of(w, k); }
+};
+template <>
+struct BmWord<8> {
+    uint32_t lo, hi;
+    __device__ __forceinline__ uint32_t byte(int k) const { return k < 4 ? byte_of(lo, k) : byte_of(hi, k - 4); }
+};
+
+// P(Y, X) = ptop(X) + Lacc(Y) + Q(Y, X):
+//   ptop(X) = sum_{xs <= x' < X} V(x')  -- band's top row relative to the strip's
+//             left edge; constant through the band, kept in shared memory
+//   Lacc(Y) = P(Y, xs)                  -- one value per bin, uniform over the warp
+//   Q(Y, X) = sum_{Y0 <= y < Y} count of row y in [xs, X)  -- <= (R+halo)*32*VC < 2^16,
+//             so two bins share one register (u16x2) and a row update is one add
+#ifndef K2_MINB
+#define K2_MINB 2
+#endif
+template <int NW, int KR, int VC, bool VEC>
+__global__ void __launch_bounds__(256, K2_MINB)
+k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, GridOut go,
+         TileGeom g, Scratch sc) {
+    extern __shared__ uint32_t smem[];
+    constexpr int NB = 2 * NW;
+    constexpr int G = K2_G;
+    const int nwarp = g.NWARP;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = (int)(blockIdx.x % g.nb2);
+    const int f = (int)(blockIdx.x / g.nb2);
+    const K2Smem lay = k2_smem(g, KR);
+    uint32_t *rowtot = smem + lay.rowtot;                    // [2][G][nwarp][NWp]
+    uint32_t *Lsup = smem + lay.Lsup;                        // [2][Lrows][NWp]
+    uint32_t *vtot = smem + lay.vtot;                        // [nwarp][NB]
+    uint32_t *Tsup = smem + lay.Tsup;                        // [2][NB]
+    uint32_t *ptop = smem + lay.ptop + (warp * NB * 32 + lane) * VC;  // this lane's [NB][VC] (stride 32*VC)
+    uint32_t *ring = smem + lay.ring + warp * KR * NB * 32 + lane;    // this lane's [KR][NB] (stride 32)
+
+    const int Y0 = b * g.R;
+    const int Ystore = min(Y0 + g.R - 1, g.h);
+    const int Ycomp = KR ? max(Ystore, min(Y0 + g.R + g.halo, g.h)) : Ystore;
+    const bool odd = (g.bins & 1) != 0;  // the last packed bin is padding
+    const int lo = g.Ws / VC - 1;        // last lane owning strip columns
+    const int NWp = g.NWp;
+    const int64_t pns = po.pns, pp = po.pp;
+    const int8_t *bmf = bm + (int64_t)f * bfs;
+    int32_t *plf = po.pl + (int64_t)f * po.pfs;
+    const uint32_t *Vb = sc.V + ((int64_t)f * g.nb2 + b) * g.Wc * NWp;
+    // lattice bookkeeping (integer divisions once per CTA)
+    const int ls = KR ? go.s : 1;
+    const int dR = KR ? go.cell / VC - 1 : 0;  // lanes between a cell's left and right corner
+    const int jtop = Y0 / ls;                   // grid row of the band's first owned cell
+    const int jend = KR ? min((Y0 + g.R - 1) / ls, go.ncy - 1) : -1;  // last owned grid row
+    const int lag = KR ? go.cell / ls : 0;      // lattice rows between a cell's top and bottom
+
+    for (int ss = 0; ss < g.nss; ++ss) {
+        const int s = ss * nwarp + warp;
+        const bool active = s < g.ns;
+        const bool last_warp = warp == nwarp - 1;
+        const int xs = s * g.Ws;
+        const int x = xs + VC * lane;  // pixel column of the lane's first column; P column x+1
+        const bool own = VC * lane < g.Ws;
+        const int X0 = x + 1;
+        const bool st = active && own && X0 <= g.w;
+        const bool lat_lane = KR && st && (x % ls) == 0 && x <= (go.ncx - 1) * ls;
+        const int gcol = x / ls;
+        const uint32_t *rdL = Lsup + (ss & 1) * g.Lrows * NWp;
+        uint32_t *wrL = Lsup + ((ss & 1) ^ 1) * g.Lrows * NWp;
+
+        uint32_t Q[NW][VC];
+        uint32_t Lacc[NB];
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+            for (int k = 0; k < VC; ++k) Q[w][k] = 0;
+
+        // ---- top row: ptop(X) = sum_{xs <= x' < X} V(x'); strip totals -> left edge
+        if (active) {
+            const bool vin = b > 0 && x < g.Wc;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                uint32_t v[VC];
+#pragma unroll
+                for (int k = 0; k < VC; ++k) v[k] = vin ? Vb[(int64_t)(x + k) * NWp + w] : 0u;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int n = 2 * w + h;
+                    uint32_t tot = 0;
+#pragma unroll
+                    for (int k = 0; k < VC; ++k) tot += half16(v[k], h);
+                    const uint32_t inc = warp_incl_scan(tot, lane);
+                    uint32_t run = inc - tot;
+                    uint32_t pt[VC];
+#pragma unroll
+                    for (int k = 0; k < VC; ++k) pt[k] = (run += half16(v[k], h));
+#pragma unroll
+                    for (int k = 0; k < VC; k += 4)
+                        *reinterpret_cast<uint4 *>(ptop + n * 32 * VC + k) =
+                            make_uint4(pt[k], pt[k + 1], pt[k + 2], pt[k + 3]);
+                    const uint32_t stot = __shfl_sync(FULL, inc, lo);  // strip total (own lanes)
+                    if (lane == 0) vtot[warp * NB + n] = stot;
+                }
+            }
+        }
+        __syncthreads();
+        if (active) {
+#pragma unroll
+            for (int n = 0; n < NB; ++n) {
+                uint32_t T = ss ? Tsup[(ss & 1) * NB + n] : 0u;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (q < warp) T += vtot[q * NB + n];
+                Lacc[n] = T;  // P(Y0, xs)
+            }
+        }
+        if (warp == 0 && lane < NB) {  // P(Y0, .) at the next super-strip's left edge
+            uint32_t T = ss ? Tsup[(ss & 1) * NB + lane] : 0u;
+            for (int q = 0; q < nwarp; ++q)
+                if (ss * nwarp + q < g.ns) T += vtot[q * NB + lane];
+            Tsup[((ss & 1) ^ 1) * NB + lane] = T;
+        }
+
+        // plane row pointer (plane 0, the lane's first column) of the next row to store
+        int32_t *prow = plf + (int64_t)Y0 * pp + X0;
+        auto store_row = [&]() {
+            if (s == 0 && lane == 0) {
+                // padded column X = 0; on aligned rows also the previous row's tail
+                // padding, so that sector is written whole
+                int32_t *p0 = prow - X0;
+#pragma unroll
+                for (int n = 0; n < NB; ++n) {
+                    if (n < NB - 1 || !odd) {
+                        if (VEC)
+                            asm volatile("st.global.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p0 - 7),
+                                         "r"(0)
+                                         : "memory");
+                        else
+                            *p0 = 0;
+                    }
+                    p0 += pns;
+                }
+            }
+            if (st) {
+                int32_t *p = prow;
+                const int valid = g.w - X0 + 1;
+#pragma unroll
+                for (int n = 0; n < NB; ++n) {
+                    if (n < NB - 1 || !odd) {
+                        uint32_t vals[VC];
+#pragma unroll
+                        for (int k = 0; k < VC; k += 4) {
+                            const uint4 t4 = *reinterpret_cast<const uint4 *>(ptop + n * 32 * VC + k);
+                            vals[k] = t4.x;
+                            vals[k + 1] = t4.y;
+                            vals[k + 2] = t4.z;
+                            vals[k + 3] = t4.w;
+                        }
+#pragma unroll
+                        for (int k = 0; k < VC; ++k) vals[k] += Lacc[n] + half16(Q[n >> 1][k], n & 1);
+                        store_chunk<VC>(p, vals, VEC, valid);
+                    }
+                    p += pns;
+                }
+            }
+            prow += pp;
+        };
+
+        // fused cell grid: lattice row number `li` (row Y0 + li*ls)
+        int li = 0;
+        int32_t *gptr = KR ? go.grid + (((int64_t)f * go.ncy + (jtop - lag)) * go.ncx + gcol) * g.bins : nullptr;
+        const int64_t gstep = (int64_t)go.ncx * g.bins;
+        auto lattice = [&]() {
+            const int jt = jtop - lag + li;  // grid row whose bottom edge is this lattice row
+            const bool emit = lat_lane && jt >= jtop && jt <= jend;
+            uint32_t gv[NB];
+#pragma unroll
+            for (int n = 0; n < NB; ++n) {
+                const uint32_t lv = ptop[n * 32 * VC + VC - 1] + Lacc[n] + half16(Q[n >> 1][VC - 1], n & 1);
+                const uint32_t r = __shfl_down_sync(FULL, lv, dR);
+                uint32_t l = __shfl_up_sync(FULL, lv, 1);
+                if (lane == 0) l = Lacc[n];
+                const uint32_t hcur = r - l;  // P(Yl, x + cell) - P(Yl, x)
+                gv[n] = hcur - ring[n * 32];
+#pragma unroll
+                for (int q = 0; q + 1 < KR; ++q) ring[(q * NB + n) * 32] = ring[((q + 1) * NB + n) * 32];
+                ring[((KR > 0 ? KR - 1 : 0) * NB + n) * 32] = hcur;
+            }
+            if (emit) {
+                if ((g.bins & 3) == 0) {
+#pragma unroll
+                    for (int n = 0; n + 3 < NB; n += 4)
+                        *reinterpret_cast<int4 *>(gptr + n) =
+                            make_int4((int)gv[n], (int)gv[n + 1], (int)gv[n + 2], (int)gv[n + 3]);
+                } else {
+#pragma unroll
+                    for (int n = 0; n < NB; ++n)
+                        if (n < NB - 1 || !odd) gptr[n] = (int)gv[n];
+                }
+            }
+            gptr += gstep;
+            ++li;
+        };
+
+        if (active) {
+            store_row();
+            if (KR) lattice();
+        }
+
+        const int8_t *brow = bmf + (int64_t)Y0 * bp + x;
+        const bool bin_ok = active && x < g.w;
+        const int bvalid = g.w - x;  // bytes of the lane's chunk inside the frame
+        auto load_bm = [&](int rel) -> BmWord<VC> {
+            BmWord<VC> r;
+            const bool ok = bin_ok && Y0 + rel < Ycomp;
+            if constexpr (VC == 8) {
+                uint2 v = ok ? __ldg(reinterpret_cast<const uint2 *>(brow + (int64_t)rel * bp))
+                             : make_uint2(0xffffffffu, 0xffffffffu);
+                if (bvalid < 8) {  // bytes past w count nowhere
+                    if (bvalid < 4) v.x |= 0xffffffffu << (8 * max(bvalid, 0)), v.y = 0xffffffffu;
+                    else v.y |= 0xffffffffu << (8 * (bvalid - 4));
+                }
+                r.lo = v.x;
+                r.hi = v.y;
+            } else {
+                uint32_t v = ok ? __ldg(reinterpret_cast<const uint32_t *>(brow + (int64_t)rel * bp))
+                                : 0xffffffffu;
+                if (bvalid < 4) v |= 0xffffffffu << (8 * max(bvalid, 0));
+                r.w = v;
+            }
+            return r;
+        };
+
+        BmWord<VC> nxt[G];
+#pragma unroll
+        for (int i = 0; i < G; ++i) nxt[i] = load_bm(i);
+        int latc = ls;  // rows until the next lattice row
+        for (int rel = 0; Y0 + rel < Ycomp; rel += G) {
+            const int gp = (rel / G) & 1;
+            BmWord<VC> bw[G];
+            uint32_t ex[G][NW];
+            const uint32_t *rt_rd = rowtot + gp * G * nwarp * NWp;
+            // ---- phase A: G rows of warp scans (independent) + strip totals
+            if (active) {
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    bw[i] = nxt[i];
+                    nxt[i] = load_bm(rel + G + i);  // next group in flight during this one
+                }
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    uint32_t hb[VC], one[VC];
+#pragma unroll
+                    for (int k = 0; k < VC; ++k) {
+                        const uint32_t v = bw[i].byte(k);
+                        hb[k] = v >> 1;
+                        one[k] = 1u << ((v & 1u) << 4);
+                    }
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) {
+                        uint32_t tot = 0;
+#pragma unroll
+                        for (int k = 0; k < VC; ++k) tot += hb[k] == (uint32_t)w ? one[k] : 0u;
+                        const uint32_t inc = warp_incl_scan(tot, lane);
+                        ex[i][w] = inc - tot;  // strip-exclusive count
+                        const uint32_t rt = __shfl_sync(FULL, inc, lo);
+                        if (lane == 0) rowtot[((gp * G + i) * nwarp + warp) * NWp + w] = rt;
+                    }
+                }
+            }
+            __syncthreads();
+            // ---- phase B: carries, accumulate, store, lattice
+            if (active) {
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    if (Y0 + rel + i < Ycomp) {
+                        const uint32_t *rti = rt_rd + i * nwarp * NWp;
+                        uint32_t hb[VC], one[VC];
+#pragma unroll
+                        for (int k = 0; k < VC; ++k) {
+                            const uint32_t v = bw[i].byte(k);
+                            hb[k] = v >> 1;
+                            one[k] = 1u << ((v & 1u) << 4);
+                        }
+#pragma unroll
+                        for (int w = 0; w < NW; ++w) {
+                            uint32_t L = ss ? rdL[(rel + i) * NWp + w] : 0u;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                if (q < warp) L += rti[q * NWp + w];
+                            if (last_warp && lane == 0) wrL[(rel + i) * NWp + w] = L + rti[warp * NWp + w];
+                            Lacc[2 * w] += L & 0xffffu;
+                            Lacc[2 * w + 1] += L >> 16;
+                            uint32_t run = ex[i][w];
+#pragma unroll
+                            for (int k = 0; k < VC; ++k) {
+                                run += hb[k] == (uint32_t)w ? one[k] : 0u;
+                                Q[w][k] += run;
+                            }
+                        }
+                        if (Y0 + rel + i + 1 <= Ystore) store_row();
+                        if (KR && --latc == 0) {
+                            latc = ls;
+                            lattice();
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int NW, int KR, int VC, bool VEC>
+void launch_planes_vc(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                      const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+    const size_t smem = (size_t)k2_smem_words(g, KR) * 4;
+    static size_t configured = 0;  // per instantiation
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(k_planes<NW, KR, VC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        configured = smem;
+    }
+    k_planes<NW, KR, VC, VEC><<<(unsigned)((int64_t)g.n * g.nb2), 32 * g.NWARP, smem, st>>>(
+        bm, bp, bfs, po, go, g, sc);
+}
+
+template <int NW, int KR>
+void launch_planes_kr(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                      const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+    if constexpr (NW <= 5) {
+        if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true>(bm, bp, bfs, po, go, g, sc, st);
+    }
+    if (po.vec)
+        launch_planes_vc<NW, KR, 4, true>(bm, bp, bfs, po, go, g, sc, st);
+    else
+        launch_planes_vc<NW, KR, 4, false>(bm, bp, bfs, po, go, g, sc, st);
+}
+
+template <int NW>
+void launch_planes_t(int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                   const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+    if (kr == 0)
+        launch_planes_kr<NW, 0>(bm, bp, bfs, po, go, g, sc, st);
+    else if (kr == 1)
+        launch_planes_kr<NW, 1>(bm, bp, bfs, po, go, g, sc, st);
+    else
+        launch_planes_kr<NW, 2>(bm, bp, bfs, po, go, g, sc, st);
+}
+
+
+}  // namespace hogb200

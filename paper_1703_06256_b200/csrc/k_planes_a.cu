@@ -1,0 +1,16 @@
+// k_planes_a.cu -- k_planes instantiations for NW in {1, 2, 3}.
+#include "k_planes.cuh"
+
+namespace hogb200 {
+
+void launch_planes_a(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                     const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+    switch (nw) {
+        case 1: launch_planes_t<1>(kr, bm, bp, bfs, po, go, g, sc, st); break;
+        case 2: launch_planes_t<2>(kr, bm, bp, bfs, po, go, g, sc, st); break;
+        case 3: launch_planes_t<3>(kr, bm, bp, bfs, po, go, g, sc, st); break;
+        default: break;
+    }
+}
+
+}  // namespace hogb200

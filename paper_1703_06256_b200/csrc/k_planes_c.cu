@@ -1,0 +1,15 @@
+// k_planes_c.cu -- k_planes instantiations for NW in {6, 7}.
+#include "k_planes.cuh"
+
+namespace hogb200 {
+
+void launch_planes_c(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                     const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+    switch (nw) {
+        case 6: launch_planes_t<6>(kr, bm, bp, bfs, po, go, g, sc, st); break;
+        case 7: launch_planes_t<7>(kr, bm, bp, bfs, po, go, g, sc, st); break;
+        default: break;
+    }
+}
+
+}  // namespace hogb200

@@ -1,0 +1,338 @@
+// k_window.cu -- the window stage and the pyramid: generic integral (bins >
+// 18), 4-corner cell grid, per-cell normalisation, window scores (lattice
+// correlation and generic per-window assembly), bilinear resize.
+// descriptor.py:107-195, detector.py:140-154, 202-221, integral.py:58-87.
+#include "hog_common.cuh"
+
+namespace hogb200 {
+
+// ---------------------------------------------------------------------------
+// Generic integral for bins > 18 (API completeness; the configs use 8/9/18):
+// row prefix per plane row, then column prefix in place.
+__global__ void k_generic_rows(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po,
+                               int n, int h, int w, int bins) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)n * bins * (h + 1)) return;
+    const int Y = (int)(i % (h + 1));
+    const int b = (int)((i / (h + 1)) % bins);
+    const int f = (int)(i / ((int64_t)(h + 1) * bins));
+    int32_t *rp = po.pl + (int64_t)f * po.pfs + (int64_t)b * po.pns + (int64_t)Y * po.pp;
+    rp[0] = 0;
+    int32_t run = 0;
+    const int8_t *src = bm + (int64_t)f * bfs + (int64_t)(Y - 1) * bp;
+    for (int X = 1; X <= w; ++X) {
+        if (Y > 0 && src[X - 1] == b) ++run;
+        rp[X] = run;
+    }
+}
+
+__global__ void k_generic_cols(PlaneOut po, int n, int h, int w, int bins) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)n * bins * (w + 1)) return;
+    const int X = (int)(i % (w + 1));
+    const int b = (int)((i / (w + 1)) % bins);
+    const int f = (int)(i / ((int64_t)(w + 1) * bins));
+    int32_t *cp = po.pl + (int64_t)f * po.pfs + (int64_t)b * po.pns + X;
+    int32_t run = 0;
+    for (int Y = 0; Y <= h; ++Y) {
+        run += cp[(int64_t)Y * po.pp];
+        cp[(int64_t)Y * po.pp] = run;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Generic cell grid from planes (descriptor.py:176-185): one thread per
+// (frame, cell), N_b x 4 corner reads.
+__global__ void k_cell_grid(const int32_t *__restrict__ pl, int64_t pp, int64_t pns, int64_t pfs,
+                            int n, int bins, const int32_t *__restrict__ cxs, int ncx,
+                            const int32_t *__restrict__ cys, int ncy, int cell,
+                            int32_t *__restrict__ grid) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)n * ncy * ncx) return;
+    const int ci = (int)(i % ncx);
+    const int cj = (int)((i / ncx) % ncy);
+    const int f = (int)(i / ((int64_t)ncx * ncy));
+    const int64_t x0 = cxs[ci], y0 = cys[cj], x1 = x0 + cell, y1 = y0 + cell;
+    const int32_t *p = pl + (int64_t)f * pfs;
+    int32_t *gp = grid + i * bins;
+    for (int b = 0; b < bins; ++b) {
+        const int32_t *q = p + (int64_t)b * pns;
+        gp[b] = __ldg(q + y1 * pp + x1) + __ldg(q + y0 * pp + x0) - __ldg(q + y0 * pp + x1) -
+                __ldg(q + y1 * pp + x0);
+    }
+}
+
+// descriptor.py:119-124 with block == 1: one denominator per cell.
+__global__ void k_cell_norm(const int32_t *__restrict__ grid, int64_t ncells_total, int bins,
+                            int norm, double eps_term, double *__restrict__ den) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ncells_total) return;
+    const int32_t *gp = grid + i * bins;
+    double s = 0.0;
+    for (int b = 0; b < bins; ++b) {
+        double v = (double)gp[b];
+        s = norm == 1 ? __dadd_rn(s, fabs(v)) : __dadd_rn(s, __dmul_rn(v, v));
+    }
+    den[i] = norm == 1 ? __dadd_rn(s, eps_term) : __dsqrt_rn(__dadd_rn(s, eps_term));
+}
+
+// ---------------------------------------------------------------------------
+// Window scores on a regular cell lattice (detector.py:140-154 with block = 1,
+// descriptor.py:107-124): the window at lattice origin (iy, ix) reads cells
+// (iy + cy*K, ix + cx*K), so scoring is a 2-D correlation of the cell grid
+// with the weight tensor.  fp64 throughout (SURVEY: fp32 misses 1e-5 on
+// blurred inputs).  Each thread owns SC_TY x SC_TX windows (register tile);
+// the CTA streams the grid rows it needs through shared memory as doubles
+// (normalised by the per-cell denominator when one is given: the division
+// happens once per cell, bit-exact with descriptor.py:119-124).
+constexpr int SC_TY = 4, SC_TX = 8, SC_YG = 2;  // windows per thread (y, x); warps per CTA
+constexpr int SC_COLS = 32 * SC_TX;              // window columns per CTA
+
+template <int CX>
+__global__ void __launch_bounds__(32 * SC_YG)
+k_scores_lattice(const int32_t *__restrict__ grid, const double *__restrict__ den, int ncy, int ncx,
+                 int bins, int noy, int nox, int cells_y, int K, const double *__restrict__ wts,
+                 double bias, double *__restrict__ scores) {
+    extern __shared__ double dsm[];
+    const int span = SC_COLS + (CX - 1) * K;          // grid columns a CTA touches
+    const int spad = span + span / 8 + 1;             // skewed row (1 pad double per 8)
+    double *wsm = dsm;                                // [cells_y][bins][CX]
+    double *rows = dsm + cells_y * bins * CX;         // [2][bins][spad]
+    const int tiles_x = (nox + SC_COLS - 1) / SC_COLS;
+    const int tiles_y = (noy + SC_TY * SC_YG - 1) / (SC_TY * SC_YG);
+    int bid = blockIdx.x;
+    const int tx = bid % tiles_x;
+    bid /= tiles_x;
+    const int ty = bid % tiles_y;
+    const int f = bid / tiles_y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ix0 = tx * SC_COLS, iy0 = ty * SC_TY * SC_YG;
+    const int iyw = iy0 + warp * SC_TY;               // this warp's first window row
+    const int32_t *gf = grid + (int64_t)f * ncy * ncx * bins;
+    const double *df = den ? den + (int64_t)f * ncy * ncx : nullptr;
+
+    // weights, transposed to [cy][n][cx] for broadcast reads
+    for (int i = threadIdx.x; i < cells_y * CX * bins; i += blockDim.x) {
+        const int n = i % bins, cx = (i / bins) % CX, cy = i / (bins * CX);
+        wsm[(cy * bins + n) * CX + cx] = wts[i];
+    }
+    const int r_first = iy0, r_last = min(iy0 + SC_TY * SC_YG - 1, noy - 1) + (cells_y - 1) * K;
+    auto stage = [&](int r, int buf) {
+        double *dst = rows + buf * bins * spad;
+        const int32_t *src = gf + ((int64_t)r * ncx + ix0) * bins;
+        for (int i = threadIdx.x; i < span * bins; i += blockDim.x) {
+            const int c = i / bins, n = i % bins;
+            double v = 0.0;
+            if (ix0 + c < ncx && r < ncy) {
+                v = (double)src[i];
+                if (df) v = __ddiv_rn(v, df[(int64_t)r * ncx + ix0 + c]);
+            }
+            dst[n * spad + c + c / 8] = v;
+        }
+    };
+    double acc[SC_TY][SC_TX];
+#pragma unroll
+    for (int u = 0; u < SC_TY; ++u)
+#pragma unroll
+        for (int t = 0; t < SC_TX; ++t) acc[u][t] = 0.0;
+
+    stage(r_first, 0);
+    __syncthreads();
+    const int c0 = lane * SC_TX;  // this thread's first window column within the tile
+    for (int r = r_first; r <= r_last; ++r) {
+        const int buf = (r - r_first) & 1;
+        if (r < r_last) stage(r + 1, buf ^ 1);
+        const double *row = rows + buf * bins * spad;
+        int cyu[SC_TY];  // weight row each of this thread's window rows takes from grid row r
+#pragma unroll
+        for (int u = 0; u < SC_TY; ++u) {
+            const int d = r - (iyw + u);
+            cyu[u] = (d >= 0 && d % K == 0 && d / K < cells_y) ? d / K : -1;
+        }
+        for (int n = 0; n < bins; ++n) {
+            double gs[SC_TX + (CX - 1) * 2];
+            const double *rn = row + n * spad;
+            // cells this thread's windows touch: c0 .. c0 + SC_TX - 1 + (CX-1)*K
+#pragma unroll
+            for (int j = 0; j < SC_TX + (CX - 1) * 2; ++j) {
+                const int c = c0 + j;
+                gs[j] = (j < SC_TX + (CX - 1) * K && c < span) ? rn[c + c / 8] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < SC_TY; ++u) {
+                const int cy = cyu[u];
+                if (cy < 0) continue;
+                const double *wr = wsm + (cy * bins + n) * CX;
+                double w[CX];
+#pragma unroll
+                for (int cx = 0; cx < CX; ++cx) w[cx] = wr[cx];
+                if (K == 1) {
+#pragma unroll
+                    for (int t = 0; t < SC_TX; ++t)
+#pragma unroll
+                        for (int cx = 0; cx < CX; ++cx) acc[u][t] = fma(w[cx], gs[t + cx], acc[u][t]);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < SC_TX; ++t)
+#pragma unroll
+                        for (int cx = 0; cx < CX; ++cx) acc[u][t] = fma(w[cx], gs[t + 2 * cx], acc[u][t]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < SC_TY; ++u) {
+        const int iy = iyw + u;
+        if (iy >= noy) continue;
+#pragma unroll
+        for (int t = 0; t < SC_TX; ++t) {
+            const int ix = ix0 + c0 + t;
+            if (ix < nox) scores[((int64_t)f * noy + iy) * nox + ix] = acc[u][t] + bias;
+        }
+    }
+}
+
+// descriptor.py:107-124 + detector.py:148-150.  One thread per window.
+__global__ void k_window_features(const int32_t *__restrict__ grid, int ncy, int ncx, int bins,
+                                  const int32_t *__restrict__ row_idx, int noy,
+                                  const int32_t *__restrict__ col_idx, int nox, int cells_x,
+                                  int cells_y, int block, int bstride, int norm, double eps_term,
+                                  const double *__restrict__ wts, double bias,
+                                  double *__restrict__ scores, double *__restrict__ desc, int n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)n * noy * nox) return;
+    const int ix = (int)(i % nox);
+    const int iy = (int)((i / nox) % noy);
+    const int f = (int)(i / ((int64_t)nox * noy));
+    const int32_t *gf = grid + (int64_t)f * ncy * ncx * bins;
+    const int32_t *ri = row_idx + (int64_t)iy * cells_y;
+    const int32_t *ci = col_idx + (int64_t)ix * cells_x;
+    const int bxn = (cells_x - block) / bstride + 1, byn = (cells_y - block) / bstride + 1;
+    const int D = bxn * byn * block * block * bins;
+    double *dp = desc ? desc + i * D : nullptr;
+    double score = 0.0;
+    int k = 0;
+    for (int by = 0; by < byn; ++by) {
+        for (int bx = 0; bx < bxn; ++bx) {
+            double den = 1.0;
+            if (norm) {
+                double s = 0.0;
+                for (int cy = 0; cy < block; ++cy)
+                    for (int cx = 0; cx < block; ++cx) {
+                        const int32_t *h = gf + ((int64_t)ri[by * bstride + cy] * ncx +
+                                                 ci[bx * bstride + cx]) * bins;
+                        for (int b = 0; b < bins; ++b) {
+                            double v = (double)h[b];
+                            s = norm == 1 ? __dadd_rn(s, fabs(v)) : __dadd_rn(s, __dmul_rn(v, v));
+                        }
+                    }
+                den = norm == 1 ? __dadd_rn(s, eps_term) : __dsqrt_rn(__dadd_rn(s, eps_term));
+            }
+            for (int cy = 0; cy < block; ++cy)
+                for (int cx = 0; cx < block; ++cx) {
+                    const int32_t *h = gf + ((int64_t)ri[by * bstride + cy] * ncx +
+                                             ci[bx * bstride + cx]) * bins;
+                    for (int b = 0; b < bins; ++b, ++k) {
+                        double v = (double)h[b];
+                        if (norm) v = __ddiv_rn(v, den);
+                        if (dp) dp[k] = v;
+                        if (wts) score = fma(__ldg(wts + k), v, score);
+                    }
+                }
+        }
+    }
+    if (scores) scores[i] = score + bias;
+}
+
+// detector.py:202-221.  Explicit _rn intrinsics keep numpy's separate
+// multiply/add roundings (no FMA contraction).
+__global__ void k_resize(const uint8_t *__restrict__ src, int n, int c, int h, int w, int64_t sp,
+                         int64_t scs, int64_t sfs, int nh, int nw, double ry, double rx,
+                         uint8_t *__restrict__ dst, int64_t dp, int64_t dcs, int64_t dfs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)n * c * nh * nw) return;
+    const int j = (int)(i % nw);
+    const int r = (int)((i / nw) % nh);
+    const int ch = (int)((i / ((int64_t)nw * nh)) % c);
+    const int f = (int)(i / ((int64_t)nw * nh * c));
+    double sy = __dsub_rn(__dmul_rn((double)r + 0.5, ry), 0.5);
+    sy = fmin(fmax(sy, 0.0), (double)(h - 1));
+    double sx = __dsub_rn(__dmul_rn((double)j + 0.5, rx), 0.5);
+    sx = fmin(fmax(sx, 0.0), (double)(w - 1));
+    const int y0 = (int)floor(sy), x0 = (int)floor(sx);
+    const int y1 = min(y0 + 1, h - 1), x1 = min(x0 + 1, w - 1);
+    const double fy = __dsub_rn(sy, (double)y0), fx = __dsub_rn(sx, (double)x0);
+    const double gy = __dsub_rn(1.0, fy), gx = __dsub_rn(1.0, fx);
+    const uint8_t *p = src + (int64_t)f * sfs + (int64_t)ch * scs;
+    const double a0 = (double)__ldg(p + (int64_t)y0 * sp + x0), b0 = (double)__ldg(p + (int64_t)y1 * sp + x0);
+    const double a1 = (double)__ldg(p + (int64_t)y0 * sp + x1), b1 = (double)__ldg(p + (int64_t)y1 * sp + x1);
+    const double r0 = __dadd_rn(__dmul_rn(a0, gy), __dmul_rn(b0, fy));
+    const double r1 = __dadd_rn(__dmul_rn(a1, gy), __dmul_rn(b1, fy));
+    double m = rint(__dadd_rn(__dmul_rn(r0, gx), __dmul_rn(r1, fx)));
+    m = fmin(fmax(m, 0.0), 255.0);
+    dst[(int64_t)f * dfs + (int64_t)ch * dcs + (int64_t)r * dp + j] = (uint8_t)m;
+}
+
+// ---- launchers ------------------------------------------------------------
+
+void launch_generic_integral(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po, int n,
+                             int h, int w, int bins, cudaStream_t st) {
+    k_generic_rows<<<blocks_for((int64_t)n * bins * (h + 1), 128), 128, 0, st>>>(bm, bp, bfs, po, n,
+                                                                               h, w, bins);
+    k_generic_cols<<<blocks_for((int64_t)n * bins * (w + 1), 128), 128, 0, st>>>(po, n, h, w, bins);
+}
+
+void launch_cell_grid(const int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, int n, int bins,
+                      const int32_t *cxs, int ncx, const int32_t *cys, int ncy, int cell,
+                      int32_t *grid, cudaStream_t st) {
+    k_cell_grid<<<blocks_for((int64_t)n * ncx * ncy, 128), 128, 0, st>>>(pl, pp, pns, pfs, n, bins,
+                                                                         cxs, ncx, cys, ncy, cell,
+                                                                         grid);
+}
+
+void launch_cell_norm(const int32_t *grid, int64_t tot, int bins, int norm, double eps_term,
+                      double *den, cudaStream_t st) {
+    k_cell_norm<<<blocks_for(tot, 256), 256, 0, st>>>(grid, tot, bins, norm, eps_term, den);
+}
+
+void launch_window_features(const int32_t *grid, int n, int ncy, int ncx, int bins,
+                            const int32_t *row_idx, int noy, const int32_t *col_idx, int nox,
+                            int cells_x, int cells_y, int block, int bstride, int norm,
+                            double eps_term, const double *wts, double bias, double *scores,
+                            double *desc, cudaStream_t st) {
+    const int64_t tot = (int64_t)n * noy * nox;
+    k_window_features<<<blocks_for(tot, 128), 128, 0, st>>>(grid, ncy, ncx, bins, row_idx, noy,
+                                                            col_idx, nox, cells_x, cells_y, block,
+                                                            bstride, norm, eps_term, wts, bias,
+                                                            scores, desc, n);
+}
+
+void launch_scores_lattice(const int32_t *grid, const double *den, int n, int ncy, int ncx,
+                           int bins, int noy, int nox, int cells_y, int k, const double *wts,
+                           double bias, double *scores, cudaStream_t st) {
+    const int span = SC_COLS + 7 * k;
+    const size_t smem =
+        sizeof(double) * ((size_t)cells_y * bins * 8 + 2 * (size_t)bins * (span + span / 8 + 1));
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(k_scores_lattice<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        configured = smem;
+    }
+    const int64_t blocks = (int64_t)n * ((noy + SC_TY * SC_YG - 1) / (SC_TY * SC_YG)) *
+                           ((nox + SC_COLS - 1) / SC_COLS);
+    k_scores_lattice<8><<<(unsigned)blocks, 32 * SC_YG, smem, st>>>(grid, den, ncy, ncx, bins, noy,
+                                                                     nox, cells_y, k, wts, bias,
+                                                                     scores);
+}
+
+void launch_resize(const uint8_t *src, int n, int c, int h, int w, int64_t sp, int64_t scs,
+                   int64_t sfs, int nh, int nw, double ry, double rx, uint8_t *dst, int64_t dp,
+                   int64_t dcs, int64_t dfs, cudaStream_t st) {
+    const int64_t tot = (int64_t)n * c * nh * nw;
+    k_resize<<<blocks_for(tot, 256), 256, 0, st>>>(src, n, c, h, w, sp, scs, sfs, nh, nw, ry, rx,
+                                                   dst, dp, dcs, dfs);
+}
+
+}  // namespace hogb200

@@ -3,17 +3,24 @@
 One ``HogPipeline`` owns every HBM buffer for a frame batch of one shape and
 runs LUT binning -> integral planes -> cell grid (fused into the plane
 kernel when the scan lattice is regular) -> optional per-cell normalisation
-and window scores, entirely on one CUDA stream with no host synchronisation.
-Frames are independent, so multi-GPU runs give each rank its own pipeline
-over its own frame shard (no collective).
+and window scores on the GPU, with no host synchronisation.
+
+The batch is processed in ``chunks`` frame groups on two streams: binning
+(instruction-bound, ~2 B/px of traffic) of chunk j+1 runs while the plane
+kernel (HBM-write-bound, 4*N_b B/px) of chunk j streams its planes out, so
+the binning time hides under the plane writes.  Frames are independent, so
+multi-GPU runs give each rank its own pipeline over its own frame shard (no
+collective).
 """
 from __future__ import annotations
+
+import ctypes
 
 import numpy as np
 
 from . import _native, device as D
 from .descriptor import (DescriptorGeometry, cell_lattice, descriptor_length, eps_term,
-                         window_features_device, window_origins, _NORM_CODE)
+                         window_origins, _NORM_CODE)
 from .gradient import build_lut
 
 
@@ -27,10 +34,20 @@ def regular_lattice(cell_xs, cell_ys, stride: int, cell: int, bins: int) -> bool
     return True
 
 
+def default_chunks(n: int, pixels_per_frame: int) -> int:
+    """Frame groups for the binning/plane overlap.  Measured on B200 (c2): the
+    plane kernel loses more to a co-running binning kernel than the overlap
+    saves, so the default is one chunk; HOGB200_CHUNKS overrides."""
+    import os
+
+    env = os.environ.get("HOGB200_CHUNKS")
+    return max(1, min(n, int(env))) if env else 1
+
+
 class HogPipeline:
     def __init__(self, n: int, channels: int, height: int, width: int, bins: int, *,
                  stride: int, cell: int = 8, window=(64, 128), normalization: str = "none",
-                 weights=None, bias: float = 0.0, lut=None, device=None):
+                 weights=None, bias: float = 0.0, lut=None, device=None, chunks: int | None = None):
         t = D.require_cuda()
         self.n, self.c, self.h, self.w, self.bins = n, channels, height, width, bins
         self.stride, self.cell = stride, cell
@@ -49,11 +66,22 @@ class HogPipeline:
         self.planes = D.alloc_planes(n, bins, height, width, dev)
         self.grid = t.empty((n, self.ncy, self.ncx, bins), dtype=t.int32, device=dev)
         self.lut_dev = D.lut_device(self.lut.table, dev)
-        sb = int(_native.load().hog_scratch_bytes(n, height, width, bins,
-                                                  stride if self.fused else 0,
-                                                  cell if self.fused else 0))
-        self.scratch = t.empty(max(sb, 256), dtype=t.uint8, device=dev)
-        self.scratch_bytes = sb
+        self.chunks = default_chunks(n, height * width) if chunks is None else max(1, min(chunks, n))
+        # frame ranges of the chunks, each with its own scratch (stages of
+        # different chunks run concurrently)
+        base, rem = divmod(n, self.chunks)
+        self.ranges, a = [], 0
+        for j in range(self.chunks):
+            b = a + base + (1 if j < rem else 0)
+            self.ranges.append((a, b))
+            a = b
+        self.scratch = []
+        for (a, b) in self.ranges:
+            sb = int(_native.load().hog_scratch_bytes(b - a, height, width, bins,
+                                                      stride if self.fused else 0,
+                                                      cell if self.fused else 0))
+            self.scratch.append((t.empty(max(sb, 256), dtype=t.uint8, device=dev), sb))
+        self.side = t.cuda.Stream(device=dev) if self.chunks > 1 else None
         self.cx_dev = t.as_tensor(self.cell_xs.astype(np.int32), device=dev)
         self.cy_dev = t.as_tensor(self.cell_ys.astype(np.int32), device=dev)
         self.denom = None
@@ -80,21 +108,54 @@ class HogPipeline:
             self.frames.data[..., : self.w].copy_(src, non_blocking=True)
 
     # -- the hot path -------------------------------------------------------
-    def run(self, stream=None, stage_events=None):
-        """Enqueue the whole batch on `stream` (default: current).  stage_events:
-        optional 4 recorded torch.cuda.Events bracketing binning / scans / planes."""
-        s = D.stream_handle(stream)
-        evs = None
-        if stage_events is not None:
-            import ctypes
-            evs = (ctypes.c_void_p * 4)(*[e.cuda_event for e in stage_events])
+    def _stage(self, j: int, stages: int, stream, events=None):
+        a, b = self.ranges[j]
         fr, bm, pl = self.frames, self.binmap, self.planes
-        _native.call("hog_pipeline", D.ptr(fr.data), self.n, self.c, self.h, self.w,
-                     fr.pitch, fr.cstride, fr.fstride, D.ptr(self.lut_dev), self.bins,
-                     D.ptr(bm.data), bm.pitch, bm.fstride, pl.ptr, pl.pitch, pl.nstride,
-                     pl.fstride, self.cell, self.stride, self.ncx, self.ncy,
-                     D.ptr(self.grid) if self.fused else None, D.ptr(self.scratch),
-                     self.scratch_bytes, evs, s)
+        scr, sb = self.scratch[j]
+        evs = None
+        if events is not None:
+            evs = (ctypes.c_void_p * 4)(*[e.cuda_event if e is not None else None for e in events])
+        _native.call("hog_pipeline", D.ptr(fr.data) + a * fr.fstride, b - a, self.c, self.h,
+                     self.w, fr.pitch, fr.cstride, fr.fstride, D.ptr(self.lut_dev), self.bins,
+                     D.ptr(bm.data) + a * bm.fstride, bm.pitch, bm.fstride,
+                     pl.ptr + 4 * a * pl.fstride, pl.pitch, pl.nstride, pl.fstride,
+                     self.cell, self.stride, self.ncx, self.ncy,
+                     (D.ptr(self.grid) + 4 * a * self.ncy * self.ncx * self.bins)
+                     if self.fused else None,
+                     D.ptr(scr), sb, stages, evs, D.stream_handle(stream))
+
+    def run(self, stream=None, plane_events=None):
+        """Enqueue the whole batch; results are ready in `stream` order (default:
+        current stream).  plane_events: optional per-chunk (start, end) pairs of
+        recorded torch.cuda.Events bracketing each plane-kernel launch on the
+        stream it runs on."""
+        t = D.torch()
+        main = stream if stream is not None else t.cuda.current_stream(self.device)
+        if self.chunks == 1:
+            evs = None
+            if plane_events is not None:
+                e0, e1 = plane_events[0]
+                evs = [None, None, e0, e1]
+            self._stage(0, _native.STAGE_ALL, main, evs)
+        else:
+            side = self.side
+            side.wait_stream(main)
+            for j in range(self.chunks):
+                self._stage(j, _native.STAGE_BIN | _native.STAGE_SCAN, main)
+                done = t.cuda.Event()
+                done.record(main)
+                side.wait_event(done)
+                evs = None
+                if plane_events is not None:
+                    e0, e1 = plane_events[j]
+                    evs = [None, None, e0, e1]
+                self._stage(j, _native.STAGE_PLANES, side, evs)
+            main.wait_stream(side)
+        self._post(main)
+
+    def _post(self, stream):
+        s = D.stream_handle(stream)
+        pl = self.planes
         if not self.fused:
             _native.call("hog_cell_grid", pl.ptr, self.n, self.h, self.w, self.bins, pl.pitch,
                          pl.nstride, pl.fstride, D.ptr(self.cx_dev), self.ncx,
@@ -118,7 +179,7 @@ class HogPipeline:
                          D.ptr(self.scores), None, s)
 
     def launches_per_run(self) -> int:
-        k = 5  # grad_bin + 3 scans + planes
+        k = 3 * self.chunks  # grad_bin + carry scan + planes per chunk
         k += 0 if self.fused else 1
         k += 1 if self.denom is not None else 0
         k += 1 if self.scores is not None else 0
