@@ -262,12 +262,19 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
 #pragma unroll
         for (int i = 0; i < G; ++i) nxt[i] = load_bm(i);
         int latc = ls;  // rows until the next lattice row
+        // Phase A scans one-hot counts of G rows.  With 4 columns per lane a strip
+        // row holds <= 128 pixels, so four bins share a word (u8x4) and the scan
+        // needs half the shuffles; with 8 columns per lane counts reach 256 and
+        // two bins share a word (u16x2).
+        constexpr bool S8 = VC == 4;
+        constexpr int SW = S8 ? (NB + 3) / 4 : NW;  // scanned words per row
+        constexpr int NE = G * NW;                  // carry entries per group
         for (int rel = 0; Y0 + rel < Ycomp; rel += G) {
             const int gp = (rel / G) & 1;
             BmWord<VC> bw[G];
-            uint32_t ex[G][NW];
-            const uint32_t *rt_rd = rowtot + gp * G * nwarp * NWp;
-            // ---- phase A: G rows of warp scans (independent) + strip totals
+            uint32_t ex[G][SW];
+            uint32_t *rt_grp = rowtot + gp * G * nwarp * NWp;  // [G][nwarp][NWp] (u8x4 or u16x2)
+            // ---- phase A: G rows of warp scans (independent) + strip row totals
             if (active) {
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
@@ -276,32 +283,53 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                 }
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
-                    uint32_t hb[VC], one[VC];
+                    uint32_t tot[SW];
+#pragma unroll
+                    for (int w = 0; w < SW; ++w) tot[w] = 0;
 #pragma unroll
                     for (int k = 0; k < VC; ++k) {
                         const uint32_t v = bw[i].byte(k);
-                        hb[k] = v >> 1;
-                        one[k] = 1u << ((v & 1u) << 4);
+                        const uint32_t q = S8 ? v >> 2 : v >> 1;
+                        const uint32_t one = S8 ? 1u << ((v & 3u) << 3) : 1u << ((v & 1u) << 4);
+#pragma unroll
+                        for (int w = 0; w < SW; ++w) tot[w] += q == (uint32_t)w ? one : 0u;
                     }
 #pragma unroll
-                    for (int w = 0; w < NW; ++w) {
-                        uint32_t tot = 0;
-#pragma unroll
-                        for (int k = 0; k < VC; ++k) tot += hb[k] == (uint32_t)w ? one[k] : 0u;
-                        const uint32_t inc = warp_incl_scan(tot, lane);
-                        ex[i][w] = inc - tot;  // strip-exclusive count
+                    for (int w = 0; w < SW; ++w) {
+                        const uint32_t inc = warp_incl_scan(tot[w], lane);
+                        ex[i][w] = inc - tot[w];  // strip-exclusive count (no borrow: inc >= tot per lane)
                         const uint32_t rt = __shfl_sync(FULL, inc, lo);
-                        if (lane == 0) rowtot[((gp * G + i) * nwarp + warp) * NWp + w] = rt;
+                        if (lane == 0) rt_grp[(i * nwarp + warp) * NWp + w] = rt;
                     }
                 }
             }
             __syncthreads();
             // ---- phase B: carries, accumulate, store, lattice
             if (active) {
+                // row-carry of (row i, word w) into this strip, one entry per lane:
+                // Lc = (carry left of this super-strip) + sum of the strip totals to the left
+                uint32_t Lsum[(NE + 31) / 32];
+#pragma unroll
+                for (int r = 0; r < (NE + 31) / 32; ++r) {
+                    const int e = lane + 32 * r;
+                    uint32_t L = 0, own_t = 0;
+                    if (e < NE) {
+                        const int i = e / NW, w = e % NW;
+                        L = ss ? rdL[(rel + i) * NWp + w] : 0u;
+                        const uint32_t *rq = rt_grp + i * nwarp * NWp;
+                        for (int q = 0; q <= warp; ++q) {
+                            const uint32_t t = S8 ? widen_half(rq[q * NWp + (w >> 1)], w & 1)
+                                                  : rq[q * NWp + w];
+                            if (q < warp) L += t;
+                            else own_t = t;
+                        }
+                        if (last_warp && Y0 + rel + i < Ycomp) wrL[(rel + i) * NWp + w] = L + own_t;
+                    }
+                    Lsum[r] = L;
+                }
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
                     if (Y0 + rel + i < Ycomp) {
-                        const uint32_t *rti = rt_rd + i * nwarp * NWp;
                         uint32_t hb[VC], one[VC];
 #pragma unroll
                         for (int k = 0; k < VC; ++k) {
@@ -311,14 +339,11 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                         }
 #pragma unroll
                         for (int w = 0; w < NW; ++w) {
-                            uint32_t L = ss ? rdL[(rel + i) * NWp + w] : 0u;
-#pragma unroll
-                            for (int q = 0; q < 8; ++q)
-                                if (q < warp) L += rti[q * NWp + w];
-                            if (last_warp && lane == 0) wrL[(rel + i) * NWp + w] = L + rti[warp * NWp + w];
+                            const int e = i * NW + w;
+                            const uint32_t L = __shfl_sync(FULL, Lsum[e / 32], e % 32);
                             Lacc[2 * w] += L & 0xffffu;
                             Lacc[2 * w + 1] += L >> 16;
-                            uint32_t run = ex[i][w];
+                            uint32_t run = S8 ? widen_half(ex[i][w >> 1], w & 1) : ex[i][w];
 #pragma unroll
                             for (int k = 0; k < VC; ++k) {
                                 run += hb[k] == (uint32_t)w ? one[k] : 0u;
