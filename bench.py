@@ -309,6 +309,15 @@ def main():
     px_step = world * nf * cfg.height * cfg.width
     value = px_step / (ms_per_step / 1e3) / 1e6
 
+    # diagnostic (outside the timed region): one more batch with per-stage events
+    sev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    for e in sev:
+        e.record()
+    p.run_staged(sev)
+    torch.cuda.synchronize()
+    stages_ms = {"grad_bin": sev[0].elapsed_time(sev[1]), "carry_scan": sev[1].elapsed_time(sev[2]),
+                 "planes_grid": sev[2].elapsed_time(sev[3])}
+
     peak, peak_src = measured_peak()
     plane_bytes = p.plane_kernel_bytes_per_frame() * nf
     achieved = plane_bytes / (plane_ms / 1e3) / 1e9
@@ -338,6 +347,7 @@ def main():
                        "l2": f"inputs larger than L2 ({step_bytes / 1e9:.2f} GB compulsory "
                              f"traffic per GPU per step vs 126 MB L2)",
                        "k_planes_ms_per_step": plane_ms,
+                       "stages_ms_diagnostic": stages_ms,
                        "chunks": nch,
                        "overlap": "binning of chunk j+1 runs on a second stream under the "
                                   "plane writes of chunk j",

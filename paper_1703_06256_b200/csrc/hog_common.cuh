@@ -144,7 +144,7 @@ __device__ __forceinline__ void count_cols(uint32_t bins4, uint32_t (&cc)[4][NWB
         const uint32_t q = v >> 2, one = 1u << ((v & 3u) << 3);
 #pragma unroll
         for (int w = 0; w < NWB; ++w)
-            if (q == (uint32_t)w) cc[k][w] += one;
+            cc[k][w] += q == (uint32_t)w ? one : 0u;
     }
 }
 

@@ -17,6 +17,9 @@ __global__ void __launch_bounds__(K_THREADS)
 k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs,
            const uint8_t *__restrict__ lut, int8_t *__restrict__ bm, int64_t bp, int64_t bfs,
            TileGeom g, Scratch sc) {
+    // per-lane column counters: cnt[bin (NB+1: slot NB = no bin)][column k][lane]
+    extern __shared__ uint32_t kbsm[];
+    constexpr int NB4 = 4 * NWB;  // bins rounded up to whole u8x4 words
     const int64_t wid = warp_id();
     if (wid >= (int64_t)g.n * g.nb1 * g.nc1) return;
     const int chunk = (int)(wid % g.nc1);
@@ -30,6 +33,20 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
     const int xl = inx ? x : ((g.w - 1) & ~3);
     const uint8_t *col = img + (int64_t)f * ifs + xl;
     const uint8_t *lut0 = lut + (255 * LUT_SIDE + 255);  // lut0[dx*511 + dy]
+    uint32_t *cnt = kbsm + (threadIdx.x >> 5) * (NB4 + 1) * 4 * 32 + lane;
+    const int nbin = g.bins;
+#ifndef K1_SMEM_COUNTS
+#define K1_SMEM_COUNTS 0
+#endif
+    uint32_t cc[4][NWB];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int w = 0; w < NWB; ++w) cc[k][w] = 0;
+    if (COUNTS && K1_SMEM_COUNTS) {
+#pragma unroll
+        for (int i = 0; i < (NB4 + 1) * 4; ++i) cnt[i * 32] = 0;
+    }
 
     // bytes of this lane's 4 columns that are interior pixels (1 <= x <= w-2)
     uint32_t valid = 0;
@@ -54,22 +71,18 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
             e2[ch] = has_edge ? (uint32_t)__ldg(pc + ch * ics + eoff) : 0u;
         }
     }
-    uint32_t cc[4][NWB];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int w = 0; w < NWB; ++w) cc[k][w] = 0;
     int8_t *bout = bm + (int64_t)f * bfs + (int64_t)y0 * bp + x;
+    const uint8_t *pd = rowp(y0 + 2);  // row y+2, clamped to the last row
 
     for (int y = y0; y < y1; ++y) {
         // row y+2 in flight while row y is binned
         uint32_t r3[CH], e3[CH];
-        const uint8_t *pd = rowp(y + 2);
 #pragma unroll
         for (int ch = 0; ch < CH; ++ch) {
             r3[ch] = __ldg(reinterpret_cast<const uint32_t *>(pd + ch * ics));
             e3[ch] = has_edge ? (uint32_t)__ldg(pd + ch * ics + eoff) : 0u;
         }
+        if (y + 3 < g.h) pd += ip;
         uint32_t bins4 = 0xffffffffu;
         if (y > 0 && y < g.h - 1) {
             int bdx[4], bdy[4], bmag[4];
@@ -101,7 +114,17 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
         }
         if (inx) *reinterpret_cast<uint32_t *>(bout) = bins4;
         bout += bp;
-        if (COUNTS) count_cols<NWB>(bins4, cc);
+        if (COUNTS) {
+#if K1_SMEM_COUNTS
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int slot = min((int)byte_of(bins4, k), nbin);  // NO_BIN -> spare slot
+                cnt[(slot * 4 + k) * 32] += 1;
+            }
+#else
+            count_cols<NWB>(bins4, cc);
+#endif
+        }
 #pragma unroll
         for (int ch = 0; ch < CH; ++ch) {
             r0[ch] = r1[ch];
@@ -111,7 +134,24 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
             e2[ch] = e3[ch];
         }
     }
-    if (COUNTS) store_cols<NWB>(g, sc, f, b, x, cc);
+    if (COUNTS && !K1_SMEM_COUNTS) store_cols<NWB>(g, sc, f, b, x, cc);
+    if (COUNTS && K1_SMEM_COUNTS) {
+        // C[f][b][x+k][w]: bins 4w..4w+3 of column x+k as u8x4 (counts <= R <= 240)
+        uint32_t *cp = sc.C + (((int64_t)f * g.nb1 + b) * g.Wc + x) * NWB;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+            for (int w = 0; w < NWB; ++w) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int n = 4 * w + j;
+                    if (n < nbin) word |= cnt[(n * 4 + k) * 32] << (8 * j);
+                }
+                cp[k * NWB + w] = word;
+            }
+        }
+    }
 }
 
 // K1': the same per-(band, column) counts from an existing bin map (hog_integral).
@@ -173,8 +213,10 @@ void grad_bin_t(int c, bool counts, const uint8_t *img, int64_t ip, int64_t ics,
                 const uint8_t *lut, int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g,
                 const Scratch &sc, cudaStream_t st) {
     const unsigned nb = blocks_for_warps((int64_t)g.n * g.nb1 * g.nc1);
+    const size_t smem =
+        (counts && K1_SMEM_COUNTS) ? sizeof(uint32_t) * (4 * NWB + 1) * 4 * 32 * (K_THREADS / 32) : 0;
 #define LAUNCH(CHv, CNT) \
-    k_grad_bin<CHv, NWB, CNT><<<nb, K_THREADS, 0, st>>>(img, ip, ics, ifs, lut, bm, bp, bfs, g, sc)
+    k_grad_bin<CHv, NWB, CNT><<<nb, K_THREADS, smem, st>>>(img, ip, ics, ifs, lut, bm, bp, bfs, g, sc)
     if (c == 1) {
         if (counts) LAUNCH(1, true); else LAUNCH(1, false);
     } else {

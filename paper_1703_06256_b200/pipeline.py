@@ -153,6 +153,24 @@ class HogPipeline:
             main.wait_stream(side)
         self._post(main)
 
+    def run_staged(self, events, stream=None):
+        """Diagnostic: the whole batch as one chunk with 4 recorded events
+        bracketing binning, carry scan and planes (+ grid)."""
+        t = D.torch()
+        main = stream if stream is not None else t.cuda.current_stream(self.device)
+        saved = self.ranges, self.scratch
+        if self.chunks > 1:  # one chunk needs the whole-batch scratch
+            sb = int(_native.load().hog_scratch_bytes(self.n, self.h, self.w, self.bins,
+                                                      self.stride if self.fused else 0,
+                                                      self.cell if self.fused else 0))
+            self.ranges = [(0, self.n)]
+            self.scratch = [(t.empty(max(sb, 256), dtype=t.uint8, device=self.device), sb)]
+        try:
+            self._stage(0, _native.STAGE_ALL, main, events)
+        finally:
+            self.ranges, self.scratch = saved
+        self._post(main)
+
     def _post(self, stream):
         s = D.stream_handle(stream)
         pl = self.planes
