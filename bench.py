@@ -232,6 +232,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1703_06256_b200 as H
+    from paper_1703_06256_b200 import sharding
     from paper_1703_06256_b200.errors import PathMismatch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -253,7 +254,7 @@ def main():
         return t.tolist()
 
     nf = args.frames or cfg.frames
-    first = rank * nf  # each rank: its own shard of distinct frames
+    first = sharding.shard(rank, world, nf).start  # each rank: its own shard of distinct frames
     frames = gen_frames(cfg, first, nf)
     weights, bias = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
     p = H.HogPipeline(nf, cfg.channels, cfg.height, cfg.width, cfg.bins, stride=cfg.stride,
