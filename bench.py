@@ -358,11 +358,13 @@ def main():
                          "traffic": traffic, "peak_source": peak_src,
                          "alg_bytes_per_launch": plane_bytes / nch, "launches_per_step": nch,
                          "alg_bytes_def": "bin map read (1 B/px) + int32 planes written "
-                                          "(4*N_b*(H+1)*(W+1)) + int32 cell grid written"},
+                                          "(4*N_b*(H+1)*(W+1)) + cell grid written "
+                                          f"({p.grid.dtype}, {p.grid.element_size()} B/bin)"},
             "pipeline_roofline": {"achieved": step_gbs, "peak": peak, "unit": "GB/s",
                                   "frac": step_gbs / peak,
                                   "alg_bytes_per_step": step_bytes,
-                                  "alg_bytes_def": "SURVEY 8d bytes_alg per frame x frames"},
+                                  "alg_bytes_def": "SURVEY 8d bytes_alg per frame x frames "
+                                                   f"(cell grid {p.grid.dtype})"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": p.launches_per_run() * K,

@@ -52,6 +52,7 @@ typedef struct CUstream_st *hog_stream_t; /* == cudaStream_t */
 #define HOG_STAGE_SCAN 2   /* column counts above every band                  */
 #define HOG_STAGE_PLANES 4 /* integral planes (+ fused cell grid)             */
 #define HOG_STAGE_ALL 7
+#define HOG_STAGE_GRID_U8 8 /* flag: the fused grid is uint8 (cell counts <= cell^2 <= 255) */
 
 /* Library version string, e.g. "hogb200 1.0 sm_100a". */
 const char *hog_version(void);
@@ -88,7 +89,8 @@ int hog_integral(const int8_t *binmap, int n, int h, int w, int64_t bm_pitch, in
  * `stride` up to ((ncx-1)*stride, (ncy-1)*stride)).  grid may be NULL (no
  * cell grid).  Requires stride % 4 == 0, cell % stride == 0, cell/stride <= 2
  * when grid != NULL; otherwise use hog_integral + hog_cell_grid.
- * stages: HOG_STAGE_* bitmask (0 = all).  A caller may run the stages of one
+ * stages: HOG_STAGE_* bitmask (0 = all), optionally | HOG_STAGE_GRID_U8: `grid`
+ * then points to uint8 [n][ncy][ncx][bins] (exact: a cell count is <= cell*cell).  A caller may run the stages of one
  * frame batch as separate calls on different streams (stage order per batch,
  * same scratch), e.g. to bin batch j+1 while batch j writes its planes.
  * stage_events: NULL, or 4 cudaEvent_t recorded on `stream` before the

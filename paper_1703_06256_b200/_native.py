@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HOGB200_LIB") or os.path.join(_HERE, "libhogb200.so")
 
 HOG_OK, HOG_EINVAL, HOG_ECUDA = 0, 1, 2
-STAGE_BIN, STAGE_SCAN, STAGE_PLANES, STAGE_ALL = 1, 2, 4, 7
+STAGE_BIN, STAGE_SCAN, STAGE_PLANES, STAGE_ALL, STAGE_GRID_U8 = 1, 2, 4, 7, 8
 
 # (name, restype, argtypes) -- must match include/hogb200.h
 _P, _I, _L, _D, _SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t

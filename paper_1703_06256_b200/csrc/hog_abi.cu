@@ -147,7 +147,7 @@ int integral_impl(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w
     if (scratch == nullptr || sbytes < need)
         return fail(HOG_EINVAL, "scratch too small: need %zu bytes, got %zu", need, sbytes);
     carve(g, scratch, &sc);
-    GridOut go{nullptr, 4, 4, 1, 1};
+    GridOut go{nullptr, 4, 4, 1, 1, 0};
     launch_counts_from_bm(g.NW, bm, bp, bfs, g, sc, st);
     launch_scan(g.NW, g, sc, st);
     launch_planes(g.NW, 0, bm, bp, bfs, po, go, g, sc, st);
@@ -216,7 +216,7 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
                  int ncy, int32_t *grid, void *scratch, size_t sbytes, int stages,
                  void *const *stage_events, hog_stream_t stream) {
     g_err.clear();
-    if (stages == 0) stages = HOG_STAGE_ALL;
+    if ((stages & HOG_STAGE_ALL) == 0) stages |= HOG_STAGE_ALL;
     int e;
     if ((e = check_frames(n, h, w)) || (e = check_bins(bins))) return e;
     if (c != 1 && c != 3) return fail(HOG_EINVAL, "channels must be 1 or 3, got %d", c);
@@ -245,7 +245,10 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
     if (scratch == nullptr || sbytes < need)
         return fail(HOG_EINVAL, "scratch too small: need %zu bytes, got %zu", need, sbytes);
     carve(g, scratch, &sc);
-    GridOut go{grid, kr ? stride : 4, kr ? cell : 4, kr ? ncx : 1, kr ? ncy : 1};
+    GridOut go{grid, kr ? stride : 4, kr ? cell : 4, kr ? ncx : 1, kr ? ncy : 1,
+               (stages & HOG_STAGE_GRID_U8) ? 1 : 0};
+    if (go.u8 && cell * cell > 255)
+        return fail(HOG_EINVAL, "uint8 cell grid needs cell*cell <= 255 (cell %d)", cell);
     auto mark = [&](int i) {
         if (stage_events && stage_events[i]) cudaEventRecord((cudaEvent_t)stage_events[i], st);
     };

@@ -78,8 +78,9 @@ struct PlaneOut {
 };
 
 struct GridOut {
-    int32_t *grid;
+    int32_t *grid;  // int32 cells, or uint8 cells when u8 (addressed in elements either way)
     int s, cell, ncx, ncy;
+    int u8;
 };
 
 constexpr int K2_G = 4;  // rows per phase-A/phase-B group

@@ -214,7 +214,20 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                 ring[((KR > 0 ? KR - 1 : 0) * NB + n) * 32] = hcur;
             }
             if (emit) {
-                if ((g.bins & 3) == 0) {
+                if (go.u8) {  // cell counts <= cell^2 <= 255: one byte per bin
+                    uint8_t *gp8 = reinterpret_cast<uint8_t *>(go.grid) + (gptr - go.grid);
+                    if ((g.bins & 3) == 0) {
+#pragma unroll
+                        for (int n = 0; n + 3 < NB; n += 4)
+                            *reinterpret_cast<uint32_t *>(gp8 + n) =
+                                __byte_perm(__byte_perm(gv[n], gv[n + 1], 0x0040),
+                                            __byte_perm(gv[n + 2], gv[n + 3], 0x0040), 0x5410);
+                    } else {
+#pragma unroll
+                        for (int n = 0; n < NB; ++n)
+                            if (n < NB - 1 || !odd) gp8[n] = (uint8_t)gv[n];
+                    }
+                } else if ((g.bins & 3) == 0) {
 #pragma unroll
                     for (int n = 0; n + 3 < NB; n += 4)
                         *reinterpret_cast<int4 *>(gptr + n) =

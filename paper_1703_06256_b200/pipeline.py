@@ -47,7 +47,8 @@ def default_chunks(n: int, pixels_per_frame: int) -> int:
 class HogPipeline:
     def __init__(self, n: int, channels: int, height: int, width: int, bins: int, *,
                  stride: int, cell: int = 8, window=(64, 128), normalization: str = "none",
-                 weights=None, bias: float = 0.0, lut=None, device=None, chunks: int | None = None):
+                 weights=None, bias: float = 0.0, lut=None, device=None, chunks: int | None = None,
+                 grid_dtype: str = "auto"):
         t = D.require_cuda()
         self.n, self.c, self.h, self.w, self.bins = n, channels, height, width, bins
         self.stride, self.cell = stride, cell
@@ -64,7 +65,16 @@ class HogPipeline:
         self.frames = D.alloc_frames(n, channels, height, width, dev)
         self.binmap = D.alloc_binmap(n, height, width, dev)
         self.planes = D.alloc_planes(n, bins, height, width, dev)
-        self.grid = t.empty((n, self.ncy, self.ncx, bins), dtype=t.int32, device=dev)
+        # the fused grid is stored as uint8 when nothing downstream on the device
+        # reads it (cell counts <= cell^2 <= 255: exact, 4x fewer grid bytes)
+        u8_ok = self.fused and cell * cell <= 255 and weights is None and normalization == "none"
+        if grid_dtype not in ("auto", "int32", "uint8"):
+            raise ValueError("grid_dtype must be 'auto', 'int32' or 'uint8'")
+        if grid_dtype == "uint8" and not u8_ok:
+            raise ValueError("uint8 grid needs a fused lattice, cell*cell <= 255 and no device scores")
+        self.grid_u8 = grid_dtype == "uint8" or (grid_dtype == "auto" and u8_ok)
+        self.grid = t.empty((n, self.ncy, self.ncx, bins),
+                            dtype=t.uint8 if self.grid_u8 else t.int32, device=dev)
         self.lut_dev = D.lut_device(self.lut.table, dev)
         self.chunks = default_chunks(n, height * width) if chunks is None else max(1, min(chunks, n))
         # frame ranges of the chunks, each with its own scratch (stages of
@@ -120,9 +130,10 @@ class HogPipeline:
                      D.ptr(bm.data) + a * bm.fstride, bm.pitch, bm.fstride,
                      pl.ptr + 4 * a * pl.fstride, pl.pitch, pl.nstride, pl.fstride,
                      self.cell, self.stride, self.ncx, self.ncy,
-                     (D.ptr(self.grid) + 4 * a * self.ncy * self.ncx * self.bins)
+                     (D.ptr(self.grid) + self.grid.element_size() * a * self.ncy * self.ncx * self.bins)
                      if self.fused else None,
-                     D.ptr(scr), sb, stages, evs, D.stream_handle(stream))
+                     D.ptr(scr), sb, stages | (_native.STAGE_GRID_U8 if self.grid_u8 else 0), evs,
+                     D.stream_handle(stream))
 
     def run(self, stream=None, plane_events=None):
         """Enqueue the whole batch; results are ready in `stream` order (default:
@@ -225,7 +236,8 @@ class HogPipeline:
     def bytes_alg_per_frame(self) -> int:
         """SURVEY §8d compulsory bytes per frame."""
         H, W, C, nb = self.h, self.w, self.c, self.bins
-        b = C * H * W + H * W + 4 * nb * (H + 1) * (W + 1) + 4 * nb * self.ncx * self.ncy
+        b = C * H * W + H * W + 4 * nb * (H + 1) * (W + 1)
+        b += self.grid.element_size() * nb * self.ncx * self.ncy
         if self.scores is not None:
             b += 8 * len(self.oxs) * len(self.oys)
         if self.denom is not None:
@@ -237,5 +249,5 @@ class HogPipeline:
         H, W, nb = self.h, self.w, self.bins
         b = H * W + 4 * nb * (H + 1) * (W + 1)
         if self.fused:
-            b += 4 * nb * self.ncx * self.ncy
+            b += self.grid.element_size() * nb * self.ncx * self.ncy
         return b

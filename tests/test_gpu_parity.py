@@ -158,7 +158,12 @@ def test_fused_grid_equals_generic_corner_reads():
     from paper_1703_06256_b200.descriptor import cell_grid_device
 
     generic = cell_grid_device(p.planes, p.cell_xs, p.cell_ys, 8)
-    assert torch.equal(generic, p.grid)
+    assert p.grid.dtype == torch.uint8  # unscored c2: exact uint8 cell counts
+    assert torch.equal(generic, p.grid.to(torch.int32))
+    q = H.HogPipeline(4, 1, cfg.height, cfg.width, cfg.bins, stride=cfg.stride, grid_dtype="int32")
+    q.upload(frames)
+    q.run()
+    assert torch.equal(generic, q.grid)
 
 
 @pytest.mark.parametrize("w,h,c,bins", [(3, 3, 1, 8), (5, 4, 3, 9), (37, 29, 1, 8),
