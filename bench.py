@@ -41,7 +41,7 @@ def parse_args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--frames", type=int, default=0, help="override frames per GPU (debug)")
     ap.add_argument("--chunks", type=int, default=0, help="override binning/plane overlap chunks")
@@ -257,6 +257,9 @@ def main():
     first = sharding.shard(rank, world, nf).start  # each rank: its own shard of distinct frames
     frames = gen_frames(cfg, first, nf)
     weights, bias = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
+    if cfg.pyramid_step:
+        return bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
+                             barrier, max_over_ranks)
     p = H.HogPipeline(nf, cfg.channels, cfg.height, cfg.width, cfg.bins, stride=cfg.stride,
                       normalization=cfg.normalization, weights=weights, bias=bias, device=dev,
                       chunks=args.chunks or None)
@@ -373,6 +376,85 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local, barrier,
+                  max_over_ranks):
+    """Config c5: every frame scanned over its 20-level pyramid (detector.py:224-269).
+    Mpixel/s counts source pixels; pyramid-level pixels are reported beside."""
+    import torch
+
+    import paper_1703_06256_b200 as H
+    from oracle import oracle as O
+    from paper_1703_06256_b200.errors import PathMismatch
+
+    p = H.PyramidPipeline(nf, cfg.channels, cfg.height, cfg.width, cfg.bins, stride=cfg.stride,
+                          scale_step=cfg.pyramid_step, weights=weights, bias=bias,
+                          chunk=min(4, nf), device=dev)
+    p.upload(frames)
+    p.run()
+    torch.cuda.synchronize()
+    # parity gate: the three smallest levels of frame 0 against the oracle
+    g = O.Geometry(64, 128, 8, 1, 1, cfg.bins)
+    lut = O.build_lut(cfg.bins)
+    for (level, factor, lw, lh) in p.levels[-3:]:
+        img = O.resize_bilinear(frames[0], lw, lh)
+        ref = O.scan_scores(O.integral_stack(O.gradient_map(img, lut), cfg.bins), g, cfg.stride,
+                            weights, bias)
+        got = p.scores[level][0].cpu().numpy()
+        if (np.abs(got - ref) > 1e-5 * np.abs(ref) + 1e-12).any():
+            raise PathMismatch(f"pyramid level {level} scores differ from the oracle")
+    K, W = args.steps, args.warmup
+    for _ in range(W):
+        p.run()
+    torch.cuda.synchronize()
+    pev = []
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    start.record()
+    for _ in range(K):
+        p.run(plane_events=pev)
+    end.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    barrier()
+    total_ms = start.elapsed_time(end)
+    plane_ms = sum(e0.elapsed_time(e1) for e0, e1, _ in pev)
+    plane_bytes = sum(b for _, _, b in pev)
+    total_ms, plane_ms = max_over_ranks([total_ms, plane_ms])
+    ms = total_ms / K
+    src_px = world * nf * cfg.height * cfg.width
+    lvl_px = world * nf * p.pixels_per_frame()
+    peak, peak_src = measured_peak()
+    achieved = plane_bytes / (plane_ms / 1e3) / 1e9
+    step_bytes = p.bytes_alg_per_frame() * nf
+    if rank == 0:
+        line = {
+            "metric": "Mpixel/s (LUT binning + per-bin integral planes + window HOG)",
+            "value": src_px / (ms / 1e3) / 1e6, "unit": "Mpixel/s (source pixels)",
+            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int32+f64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg), "frames_per_gpu": nf,
+                       "levels": len(p.levels), "level_mpixel_per_s": lvl_px / (ms / 1e3) / 1e6,
+                       "frames_per_chunk": p.chunk,
+                       "parallelism": f"frame-sharded x{world}, no collective",
+                       "l2": f"inputs larger than L2 ({step_bytes / 1e9:.1f} GB per GPU per step)"},
+            "roofline": {"bound": "hbm", "kernel": "k_planes", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "peak_source": peak_src, "launches_per_step": len(pev) // K,
+                         "alg_bytes_per_step": plane_bytes / K},
+            "pipeline_roofline": {"achieved": step_bytes / (ms / 1e3) / 1e9, "peak": peak,
+                                  "unit": "GB/s", "frac": step_bytes / (ms / 1e3) / 1e9 / peak,
+                                  "alg_bytes_per_step": step_bytes},
+            "cpu_baseline": None, "e2e": None,
+            "gpu_launches": p.launches_per_run() * K, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
     return 0
 
 

@@ -251,3 +251,125 @@ class HogPipeline:
         if self.fused:
             b += self.grid.element_size() * nb * self.ncx * self.ncy
         return b
+
+
+def pyramid_levels(width: int, height: int, window_w: int, window_h: int, scale_step: float):
+    """detector.py:251-257: [(level, factor, w, h)] while the window fits."""
+    out, level = [], 0
+    while True:
+        factor = scale_step ** level
+        w = int(width / factor)
+        h = int(height / factor)
+        if w < window_w or h < window_h:
+            break
+        out.append((level, factor, w, h))
+        level += 1
+    return out
+
+
+class PyramidPipeline:
+    """Multi-scale scan of a frame batch (detector.py:224-269), on the device.
+
+    Every level is resized from the ORIGINAL frame (detector.py:258) by
+    ``hog_resize_bilinear`` and then runs a level ``HogPipeline`` (binning,
+    planes, cell grid, scores).  Frames go through in chunks of ``chunk``
+    so the per-level buffers (planes: 4*N_b B/px) are reused; every level's
+    score map of every frame is kept (``scores[level]``: (N, noy, nox) f64).
+    """
+
+    def __init__(self, n: int, channels: int, height: int, width: int, bins: int, *,
+                 stride: int, scale_step: float, weights, bias: float = 0.0, cell: int = 8,
+                 window=(64, 128), chunk: int = 4, device=None, lut=None):
+        t = D.require_cuda()
+        if scale_step <= 1.0:
+            raise ValueError(f"scale_step must be > 1, got {scale_step}")
+        self.n, self.c, self.h, self.w, self.bins = n, channels, height, width, bins
+        self.chunk = max(1, min(chunk, n))
+        self.device = t.device(device or "cuda")
+        self.lut = lut or build_lut(bins)
+        self.levels = pyramid_levels(width, height, window[0], window[1], scale_step)
+        if not self.levels:
+            from .errors import WindowLargerThanImage
+
+            raise WindowLargerThanImage(
+                f"window {window[0]}x{window[1]} exceeds image {width}x{height}")
+        self.src = D.alloc_frames(n, channels, height, width, self.device)
+        self.pipes = [HogPipeline(self.chunk, channels, h, w, bins, stride=stride, cell=cell,
+                                  window=window, weights=weights, bias=bias, lut=self.lut,
+                                  device=self.device)
+                      for (_, _, w, h) in self.levels]
+        self.scores = [t.empty((n,) + tuple(p.scores.shape[1:]), dtype=t.float64,
+                               device=self.device) for p in self.pipes]
+
+    def upload(self, frames: np.ndarray):
+        t = D.torch()
+        src = t.from_numpy(np.ascontiguousarray(frames))
+        if self.src.pitch == self.w:
+            self.src.data.copy_(src, non_blocking=True)
+        else:
+            self.src.data[..., : self.w].copy_(src, non_blocking=True)
+
+    def run(self, stream=None, plane_events=None):
+        """plane_events: optional list; (start, end, algorithmic bytes) of every
+        plane-kernel launch is appended (events recorded on the launch stream)."""
+        t = D.torch()
+        main = stream if stream is not None else t.cuda.current_stream(self.device)
+        s = D.stream_handle(main)
+        src = self.src
+        for a in range(0, self.n, self.chunk):
+            m = min(self.chunk, self.n - a)
+            for (level, factor, w, h), p in zip(self.levels, self.pipes):
+                dst = p.frames
+                if level == 0:
+                    dst.data[:m].copy_(src.data[a:a + m])
+                else:
+                    _native.call("hog_resize_bilinear", D.ptr(src.data) + a * src.fstride, m,
+                                 self.c, self.h, self.w, src.pitch, src.cstride, src.fstride, h, w,
+                                 self.h / h, self.w / w, D.ptr(dst.data), dst.pitch, dst.cstride,
+                                 dst.fstride, s)
+                pev = None
+                if plane_events is not None:
+                    pev = []
+                    for _ in range(p.chunks):
+                        e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+                        e0.record(main)
+                        e1.record(main)
+                        pev.append((e0, e1))
+                        plane_events.append((e0, e1, p.plane_kernel_bytes_per_frame() * p.n // p.chunks))
+                p.run(main, plane_events=pev)
+                self.scores[level][a:a + m].copy_(p.scores[:m])
+
+    def pixels_per_frame(self) -> int:
+        """Pixels of every pyramid level of one frame."""
+        return sum(w * h for (_, _, w, h) in self.levels)
+
+    def bytes_alg_per_frame(self) -> int:
+        """SURVEY §8d for c5: per level bytes_alg, plus the resize (w*h written,
+        min(H, 2h)*W source rows read) for levels >= 1."""
+        b = 0
+        for (level, _, w, h), p in zip(self.levels, self.pipes):
+            b += p.bytes_alg_per_frame()
+            if level:
+                b += self.c * (w * h + min(self.h, 2 * h) * self.w)
+        return b
+
+    def launches_per_run(self) -> int:
+        per_chunk = sum(p.launches_per_run() + (1 if lv else 0)
+                        for (lv, _, _, _), p in zip(self.levels, self.pipes))
+        return per_chunk * ((self.n + self.chunk - 1) // self.chunk)
+
+    def detections(self, frame: int, threshold: float, window=(64, 128)):
+        """Host boxes of one frame, as pyramid_scan returns them (detector.py:252-268)."""
+        from .detector import Detection
+
+        out = []
+        for (level, factor, w, h), p in zip(self.levels, self.pipes):
+            sc = self.scores[level][frame].cpu().numpy()
+            ww, wh = int(round(window[0] * factor)), int(round(window[1] * factor))
+            iy, ix = np.nonzero(sc > threshold)
+            for j, i in zip(iy.tolist(), ix.tolist()):
+                x = min(max(int(round(int(p.oxs[i]) * factor)), 0), self.w - 1)
+                y = min(max(int(round(int(p.oys[j]) * factor)), 0), self.h - 1)
+                out.append(Detection(x=x, y=y, w=min(ww, self.w - x), h=min(wh, self.h - y),
+                                     score=float(sc[j, i]), scale=factor))
+        return out
