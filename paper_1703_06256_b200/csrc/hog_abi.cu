@@ -92,12 +92,14 @@ size_t carve(const TileGeom &g, void *base, Scratch *sc) {
         off += round_up((int64_t)bytes, 256);
         return o;
     };
-    size_t oC = take(sizeof(uint32_t) * (size_t)g.n * g.nb1 * g.Wc * g.NWB);
+    size_t oC = take(sizeof(uint32_t) * (size_t)g.n * g.nb2 * g.Wc * g.NWB);
     size_t oV = take(sizeof(uint32_t) * (size_t)g.n * g.nb2 * g.Wc * g.NWp);
+    size_t oF = take(sizeof(uint32_t) * ((size_t)g.n * g.nb2 + 1));
     if (sc && base) {
         char *b = (char *)base;
         sc->C = (uint32_t *)(b + oC);
         sc->V = (uint32_t *)(b + oV);
+        sc->flags = (uint32_t *)(b + oF);
     }
     return off;
 }
@@ -150,7 +152,7 @@ int integral_impl(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w
     GridOut go{nullptr, 4, 4, 1, 1, 0};
     launch_counts_from_bm(g.NW, bm, bp, bfs, g, sc, st);
     launch_scan(g.NW, g, sc, st);
-    launch_planes(g.NW, 0, bm, bp, bfs, po, go, g, sc, st);
+    launch_planes(g.NW, 0, 0, bm, bp, bfs, po, go, g, sc, FusedIn{}, st);
     return check_launch("hog_integral");
 }
 
@@ -252,14 +254,33 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
     auto mark = [&](int i) {
         if (stage_events && stage_events[i]) cudaEventRecord((cudaEvent_t)stage_events[i], st);
     };
-    mark(0);
-    if (stages & HOG_STAGE_BIN)
-        launch_grad_bin(g.NWB, c, true, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st);
-    mark(1);
-    if (stages & HOG_STAGE_SCAN) launch_scan(g.NW, g, sc, st);
-    mark(2);
-    if (stages & HOG_STAGE_PLANES) launch_planes(g.NW, kr, bm, bp, bfs, po, go, g, sc, st);
-    mark(3);
+    // Opt-in (HOGB200_FUSED=1): the fused plane kernel bins its own rows and
+    // takes the band carries by decoupled look-back (no k_grad_bin /
+    // k_scan_cols passes).  Measured slower on B200 (c2: 1.73 vs 1.29 ms per
+    // step): binning is latency-bound and starves at the plane kernel's
+    // occupancy, so the default is the three-kernel path.
+    const char *fenv = getenv("HOGB200_FUSED");
+    const bool fused = (stages & HOG_STAGE_ALL) == HOG_STAGE_ALL && g.nss == 1 && po.vec &&
+                       fenv && fenv[0] == '1';
+    if (fused) {
+        FusedIn fi{img, ip, ics, ifs, lut, sc.flags, sc.flags + (size_t)g.n * g.nb2};
+        cudaMemsetAsync(sc.flags, 0, sizeof(uint32_t) * ((size_t)g.n * g.nb2 + 1), st);
+        mark(0);
+        mark(1);
+        mark(2);
+        launch_planes(g.NW, kr, c, bm, bp, bfs, po, go, g, sc, fi, st);
+        mark(3);
+    } else {
+        mark(0);
+        if (stages & HOG_STAGE_BIN)
+            launch_grad_bin(g.NWB, c, true, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st);
+        mark(1);
+        if (stages & HOG_STAGE_SCAN) launch_scan(g.NW, g, sc, st);
+        mark(2);
+        if (stages & HOG_STAGE_PLANES)
+            launch_planes(g.NW, kr, 0, bm, bp, bfs, po, go, g, sc, FusedIn{}, st);
+        mark(3);
+    }
     return check_launch("hog_pipeline");
 }
 

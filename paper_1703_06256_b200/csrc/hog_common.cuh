@@ -47,8 +47,10 @@ struct TileGeom {
 
 // Scratch arrays (device), carved from the caller's scratch buffer.
 struct Scratch {
-    uint32_t *C;  // [n][nb1][Wc][NWB]  bin counts per (pixel band, column), u8x4
-    uint32_t *V;  // [n][nb2][Wc][NWp]  counts above each plane band, u16x2
+    uint32_t *C;      // [n][nb2][Wc][NWB]  bin counts per (pixel band, column), u8x4
+    uint32_t *V;      // [n][nb2][Wc][NWp]  counts above each plane band, u16x2
+                      //   (fused: counts above band b+1, published by band b)
+    uint32_t *flags;  // [n][nb2] + 1 ticket: fused look-back state (zeroed per launch)
 };
 
 
@@ -84,6 +86,26 @@ struct GridOut {
 };
 
 constexpr int K2_G = 4;  // rows per phase-A/phase-B group
+
+// Inputs of the fused plane kernel (binning inside k_planes, band carries by
+// decoupled look-back instead of k_grad_bin counts + k_scan_cols).
+struct FusedIn {
+    const uint8_t *img;
+    int64_t ip, ics, ifs;
+    const uint8_t *lut;
+    uint32_t *flags;   // [n][nb2]: 0 none, 1 band aggregate published, 2 inclusive published
+    uint32_t *ticket;  // CTA ticket counter (zeroed with the flags before every launch)
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // shared-memory carve-up of one k_planes CTA (32-bit words, every array 16-B aligned)
 struct K2Smem {
@@ -174,21 +196,26 @@ void launch_counts_from_bm(int nw, const int8_t *bm, int64_t bp, int64_t bfs, co
                            const Scratch &sc, cudaStream_t st);
 void launch_scan(int nw, const TileGeom &g, const Scratch &sc, cudaStream_t st);
 // k_planes_*.cu
-void launch_planes_a(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
-                     const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st);
-void launch_planes_b(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
-                     const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st);
-void launch_planes_c(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
-                     const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st);
-void launch_planes_d(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
-                     const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st);
-inline void launch_planes(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs,
+void launch_planes_a(int nw, int kr, int ch, const int8_t *bm, int64_t bp, int64_t bfs,
+                     const PlaneOut &po, const GridOut &go, const TileGeom &g, const Scratch &sc,
+                     const FusedIn &fi, cudaStream_t st);
+void launch_planes_b(int nw, int kr, int ch, const int8_t *bm, int64_t bp, int64_t bfs,
+                     const PlaneOut &po, const GridOut &go, const TileGeom &g, const Scratch &sc,
+                     const FusedIn &fi, cudaStream_t st);
+void launch_planes_c(int nw, int kr, int ch, const int8_t *bm, int64_t bp, int64_t bfs,
+                     const PlaneOut &po, const GridOut &go, const TileGeom &g, const Scratch &sc,
+                     const FusedIn &fi, cudaStream_t st);
+void launch_planes_d(int nw, int kr, int ch, const int8_t *bm, int64_t bp, int64_t bfs,
+                     const PlaneOut &po, const GridOut &go, const TileGeom &g, const Scratch &sc,
+                     const FusedIn &fi, cudaStream_t st);
+// ch: 0 = bin map given (k_grad_bin + k_scan_cols ran), 1/3 = fused binning + look-back
+inline void launch_planes(int nw, int kr, int ch, const int8_t *bm, int64_t bp, int64_t bfs,
                           const PlaneOut &po, const GridOut &go, const TileGeom &g,
-                          const Scratch &sc, cudaStream_t st) {
-    if (nw <= 3) launch_planes_a(nw, kr, bm, bp, bfs, po, go, g, sc, st);
-    else if (nw <= 5) launch_planes_b(nw, kr, bm, bp, bfs, po, go, g, sc, st);
-    else if (nw <= 7) launch_planes_c(nw, kr, bm, bp, bfs, po, go, g, sc, st);
-    else launch_planes_d(nw, kr, bm, bp, bfs, po, go, g, sc, st);
+                          const Scratch &sc, const FusedIn &fi, cudaStream_t st) {
+    if (nw <= 3) launch_planes_a(nw, kr, ch, bm, bp, bfs, po, go, g, sc, fi, st);
+    else if (nw <= 5) launch_planes_b(nw, kr, ch, bm, bp, bfs, po, go, g, sc, fi, st);
+    else if (nw <= 7) launch_planes_c(nw, kr, ch, bm, bp, bfs, po, go, g, sc, fi, st);
+    else launch_planes_d(nw, kr, ch, bm, bp, bfs, po, go, g, sc, fi, st);
 }
 // k_window.cu
 void launch_generic_integral(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po, int n,

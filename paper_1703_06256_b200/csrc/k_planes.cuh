@@ -36,6 +36,130 @@ struct BmWord<8> {
     __device__ __forceinline__ uint32_t byte(int k) const { return k < 4 ? byte_of(lo, k) : byte_of(hi, k - 4); }
 };
 
+// Gradient + LUT binning (gradient.py:95-121) of plane-kernel rows: lane owns
+// pixel columns x .. x+VC-1 (VC/4 words).  Writes the bin map for rows
+// [y0, y1) of owned columns and counts bins of rows [y0, ycnt) per column
+// into cc (u8x4, bins 4w..4w+3 of column k in cc[k][w]).
+template <int CH, int VC, int NWB>
+__device__ __forceinline__ void bin_rows(const FusedIn &fi, const TileGeom &g, int f, int x,
+                                         int lane, bool own, int y0, int y1, int ycnt,
+                                         int8_t *bmf, int64_t bp, uint32_t (&cc)[VC][NWB]) {
+    constexpr int ND = VC / 4;
+    const uint8_t *lut0 = fi.lut + (255 * LUT_SIDE + 255);
+    const uint8_t *base = fi.img + (int64_t)f * fi.ifs;
+    const int xlast = (g.w - 1) & ~3;
+    int xo[ND];
+    uint32_t valid[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+        xo[d] = min(x + 4 * d, xlast);  // lanes past the frame re-read the last word
+        valid[d] = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (x + 4 * d + k >= 1 && x + 4 * d + k <= g.w - 2) valid[d] |= 0xffu << (8 * k);
+    }
+    const int eoff = lane == 0 ? -1 : VC;
+    const bool has_edge = (lane == 0 && x >= 1) || (lane == 31 && x + VC < g.w);
+    auto rowp = [&](int y) { return base + (int64_t)min(max(y, 0), g.h - 1) * fi.ip; };
+    uint32_t r0[CH][ND], r1[CH][ND], r2[CH][ND], e1[CH], e2[CH];
+    {
+        const uint8_t *pa = rowp(y0 - 1), *pb = rowp(y0), *pc = rowp(y0 + 1);
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+                r0[ch][d] = __ldg(reinterpret_cast<const uint32_t *>(pa + ch * fi.ics + xo[d]));
+                r1[ch][d] = __ldg(reinterpret_cast<const uint32_t *>(pb + ch * fi.ics + xo[d]));
+                r2[ch][d] = __ldg(reinterpret_cast<const uint32_t *>(pc + ch * fi.ics + xo[d]));
+            }
+            e1[ch] = has_edge ? (uint32_t)__ldg(pb + ch * fi.ics + x + eoff) : 0u;
+            e2[ch] = has_edge ? (uint32_t)__ldg(pc + ch * fi.ics + x + eoff) : 0u;
+        }
+    }
+    const uint8_t *pd = rowp(y0 + 2);
+    int8_t *bout = bmf + (int64_t)y0 * bp + x;
+    for (int y = y0; y < y1; ++y) {
+        uint32_t r3[CH][ND], e3[CH];
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+#pragma unroll
+            for (int d = 0; d < ND; ++d)
+                r3[ch][d] = __ldg(reinterpret_cast<const uint32_t *>(pd + ch * fi.ics + xo[d]));
+            e3[ch] = has_edge ? (uint32_t)__ldg(pd + ch * fi.ics + x + eoff) : 0u;
+        }
+        if (y + 3 < g.h) pd += fi.ip;
+        uint32_t bins[ND];
+#pragma unroll
+        for (int d = 0; d < ND; ++d) bins[d] = 0xffffffffu;
+        if (y > 0 && y < g.h - 1) {
+            int bdx[ND][4], bdy[ND][4], bmag[ND][4];
+#pragma unroll
+            for (int ch = 0; ch < CH; ++ch) {
+                const uint32_t prev = __shfl_up_sync(FULL, r1[ch][ND - 1], 1);
+                const uint32_t next = __shfl_down_sync(FULL, r1[ch][0], 1);
+#pragma unroll
+                for (int d = 0; d < ND; ++d) {
+                    const uint32_t lb = d > 0 ? r1[ch][d - 1] >> 24 : (lane == 0 ? e1[ch] : prev >> 24);
+                    const uint32_t rb = d + 1 < ND ? r1[ch][d + 1] : (lane == 31 ? e1[ch] : next);
+                    const uint32_t Lw = __byte_perm(lb, r1[ch][d], 0x6540);  // x-1 .. x+2
+                    const uint32_t Rw = __byte_perm(r1[ch][d], rb, 0x4321);  // x+1 .. x+4
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int dx = (int)byte_of(Rw, k) - (int)byte_of(Lw, k);
+                        const int dy = (int)byte_of(r2[ch][d], k) - (int)byte_of(r0[ch][d], k);
+                        if (CH == 1) {
+                            bdx[d][k] = dx, bdy[d][k] = dy;
+                        } else {
+                            // gradient.py:113-117: largest dx^2+dy^2 wins, first channel on ties
+                            const int mag = dx * dx + dy * dy;
+                            if (ch == 0 || mag > bmag[d][k])
+                                bdx[d][k] = dx, bdy[d][k] = dy, bmag[d][k] = mag;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+                uint32_t v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[k] = __ldg(lut0 + (bdx[d][k] * LUT_SIDE + bdy[d][k]));
+                const uint32_t w4 = __byte_perm(__byte_perm(v[0], v[1], 0x0040),
+                                                __byte_perm(v[2], v[3], 0x0040), 0x5410);
+                bins[d] = (w4 & valid[d]) | ~valid[d];
+            }
+        }
+        if (own) {
+#pragma unroll
+            for (int d = 0; d < ND; ++d)
+                if (x + 4 * d < g.w) *reinterpret_cast<uint32_t *>(bout + 4 * d) = bins[d];
+            if (y < ycnt) {
+#pragma unroll
+                for (int d = 0; d < ND; ++d) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t v = byte_of(bins[d], k);
+                        const uint32_t q = v >> 2, one = 1u << ((v & 3u) << 3);
+#pragma unroll
+                        for (int w = 0; w < NWB; ++w) cc[4 * d + k][w] += q == (uint32_t)w ? one : 0u;
+                    }
+                }
+            }
+        }
+        bout += bp;
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+                r0[ch][d] = r1[ch][d];
+                r1[ch][d] = r2[ch][d];
+                r2[ch][d] = r3[ch][d];
+            }
+            e1[ch] = e2[ch];
+            e2[ch] = e3[ch];
+        }
+    }
+}
+
 // P(Y, X) = ptop(X) + Lacc(Y) + Q(Y, X):
 //   ptop(X) = sum_{xs <= x' < X} V(x')  -- band's top row relative to the strip's
 //             left edge; constant through the band, kept in shared memory
@@ -45,17 +169,28 @@ struct BmWord<8> {
 #ifndef K2_MINB
 #define K2_MINB 2
 #endif
-template <int NW, int KR, int VC, bool VEC>
+// CH > 0: fused variant -- the CTA bins its own rows from the frame (CH
+// channels) and gets the column counts above its band by decoupled look-back
+// over the bands above (tickets keep the waits acyclic); requires nss == 1.
+template <int NW, int KR, int VC, bool VEC, int CH = 0>
 __global__ void __launch_bounds__(256, K2_MINB)
 k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, GridOut go,
-         TileGeom g, Scratch sc) {
+         TileGeom g, Scratch sc, FusedIn fi) {
     extern __shared__ uint32_t smem[];
     constexpr int NB = 2 * NW;
+    constexpr int NWB = (NB + 3) / 4;
     constexpr int G = K2_G;
     const int nwarp = g.NWARP;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int b = (int)(blockIdx.x % g.nb2);
-    const int f = (int)(blockIdx.x / g.nb2);
+    __shared__ int tk;
+    int64_t bid = blockIdx.x;
+    if (CH) {
+        if (threadIdx.x == 0) tk = (int)atomicAdd(fi.ticket, 1u);
+        __syncthreads();
+        bid = tk;
+    }
+    const int b = (int)(bid % g.nb2);
+    const int f = (int)(bid / g.nb2);
     const K2Smem lay = k2_smem(g, KR);
     uint32_t *rowtot = smem + lay.rowtot;                    // [2][G][nwarp][NWp]
     uint32_t *Lsup = smem + lay.Lsup;                        // [2][Lrows][NWp]
@@ -72,6 +207,7 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
     const int NWp = g.NWp;
     const int64_t pns = po.pns, pp = po.pp;
     const int8_t *bmf = bm + (int64_t)f * bfs;
+    int8_t *bmw = const_cast<int8_t *>(bmf);
     int32_t *plf = po.pl + (int64_t)f * po.pfs;
     const uint32_t *Vb = sc.V + ((int64_t)f * g.nb2 + b) * g.Wc * NWp;
     // lattice bookkeeping (integer divisions once per CTA)
@@ -102,14 +238,88 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
 #pragma unroll
             for (int k = 0; k < VC; ++k) Q[w][k] = 0;
 
+        // column counts above the band, u16x2 (fused: binning + look-back here)
+        uint32_t vreg[NW][VC];
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+            for (int k = 0; k < VC; ++k) vreg[w][k] = 0;
+        if constexpr (CH > 0) {
+            uint32_t cc[VC][NWB];
+#pragma unroll
+            for (int k = 0; k < VC; ++k)
+#pragma unroll
+                for (int w = 0; w < NWB; ++w) cc[k][w] = 0;
+            const int yown = min(Y0 + g.R, g.h);  // pixel rows of this band
+            if (active)
+                bin_rows<CH, VC, NWB>(fi, g, f, x, lane, own, Y0, max(Ycomp, yown), yown, bmw, bp, cc);
+            // publish this band's per-column counts (aggregate)
+            uint32_t *agg = sc.C + ((int64_t)f * g.nb2 + b) * g.Wc * NWB;
+            if (active && own) {
+#pragma unroll
+                for (int k = 0; k < VC; ++k)
+                    if (x + k < g.Wc)
+#pragma unroll
+                        for (int w = 0; w < NWB; ++w) agg[(int64_t)(x + k) * NWB + w] = cc[k][w];
+            }
+            __threadfence();
+            __syncthreads();
+            uint32_t *flags = fi.flags + (int64_t)f * g.nb2;
+            if (threadIdx.x == 0) st_release_gpu(flags + b, 1u);
+            // decoupled look-back over the bands above
+            if (active) {
+                for (int q = b - 1; q >= 0; --q) {
+                    uint32_t fl = 0;
+                    if (lane == 0) {
+                        while ((fl = ld_acquire_gpu(flags + q)) == 0u) __nanosleep(64);
+                    }
+                    fl = __shfl_sync(FULL, fl, 0);
+                    __threadfence();
+                    if (fl == 2u) {
+                        const uint32_t *inc = sc.V + ((int64_t)f * g.nb2 + q) * g.Wc * NWp;
+#pragma unroll
+                        for (int k = 0; k < VC; ++k)
+                            if (x + k < g.Wc)
+#pragma unroll
+                                for (int w = 0; w < NW; ++w) vreg[w][k] += inc[(int64_t)(x + k) * NWp + w];
+                        break;
+                    }
+                    const uint32_t *ag = sc.C + ((int64_t)f * g.nb2 + q) * g.Wc * NWB;
+#pragma unroll
+                    for (int k = 0; k < VC; ++k)
+                        if (x + k < g.Wc)
+#pragma unroll
+                            for (int w = 0; w < NW; ++w)
+                                vreg[w][k] += widen_half(ag[(int64_t)(x + k) * NWB + (w >> 1)], w & 1);
+                }
+                // publish the inclusive counts (above band b+1)
+                uint32_t *incl = sc.V + ((int64_t)f * g.nb2 + b) * g.Wc * NWp;
+                if (own) {
+#pragma unroll
+                    for (int k = 0; k < VC; ++k)
+                        if (x + k < g.Wc)
+#pragma unroll
+                            for (int w = 0; w < NW; ++w)
+                                incl[(int64_t)(x + k) * NWp + w] = vreg[w][k] + widen_half(cc[k][w >> 1], w & 1);
+                }
+            }
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) st_release_gpu(flags + b, 2u);
+        } else if (active && b > 0 && x < g.Wc) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w)
+#pragma unroll
+                for (int k = 0; k < VC; ++k) vreg[w][k] = Vb[(int64_t)(x + k) * NWp + w];
+        }
+
         // ---- top row: ptop(X) = sum_{xs <= x' < X} V(x'); strip totals -> left edge
         if (active) {
-            const bool vin = b > 0 && x < g.Wc;
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
                 uint32_t v[VC];
 #pragma unroll
-                for (int k = 0; k < VC; ++k) v[k] = vin ? Vb[(int64_t)(x + k) * NWp + w] : 0u;
+                for (int k = 0; k < VC; ++k) v[k] = vreg[w][k];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int n = 2 * w + h;
@@ -376,42 +586,56 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
     }
 }
 
-template <int NW, int KR, int VC, bool VEC>
+template <int NW, int KR, int VC, bool VEC, int CH>
 void launch_planes_vc(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
-                      const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+                      const GridOut &go, const TileGeom &g, const Scratch &sc, const FusedIn &fi,
+                      cudaStream_t st) {
     const size_t smem = (size_t)k2_smem_words(g, KR) * 4;
     static size_t configured = 0;  // per instantiation
     if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(k_planes<NW, KR, VC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaFuncSetAttribute(k_planes<NW, KR, VC, VEC, CH>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = smem;
     }
-    k_planes<NW, KR, VC, VEC><<<(unsigned)((int64_t)g.n * g.nb2), 32 * g.NWARP, smem, st>>>(
-        bm, bp, bfs, po, go, g, sc);
+    k_planes<NW, KR, VC, VEC, CH><<<(unsigned)((int64_t)g.n * g.nb2), 32 * g.NWARP, smem, st>>>(
+        bm, bp, bfs, po, go, g, sc, fi);
 }
 
 template <int NW, int KR>
-void launch_planes_kr(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
-                      const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+void launch_planes_kr(int ch, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                      const GridOut &go, const TileGeom &g, const Scratch &sc, const FusedIn &fi,
+                      cudaStream_t st) {
+    if (ch == 1) {  // fused, grayscale
+        if constexpr (NW <= 5) {
+            if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 1>(bm, bp, bfs, po, go, g, sc, fi, st);
+        }
+        return launch_planes_vc<NW, KR, 4, true, 1>(bm, bp, bfs, po, go, g, sc, fi, st);
+    }
+    if (ch == 3) {  // fused, RGB
+        if constexpr (NW <= 5) {
+            if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 3>(bm, bp, bfs, po, go, g, sc, fi, st);
+        }
+        return launch_planes_vc<NW, KR, 4, true, 3>(bm, bp, bfs, po, go, g, sc, fi, st);
+    }
     if constexpr (NW <= 5) {
-        if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true>(bm, bp, bfs, po, go, g, sc, st);
+        if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 0>(bm, bp, bfs, po, go, g, sc, fi, st);
     }
     if (po.vec)
-        launch_planes_vc<NW, KR, 4, true>(bm, bp, bfs, po, go, g, sc, st);
+        launch_planes_vc<NW, KR, 4, true, 0>(bm, bp, bfs, po, go, g, sc, fi, st);
     else
-        launch_planes_vc<NW, KR, 4, false>(bm, bp, bfs, po, go, g, sc, st);
+        launch_planes_vc<NW, KR, 4, false, 0>(bm, bp, bfs, po, go, g, sc, fi, st);
 }
 
 template <int NW>
-void launch_planes_t(int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
-                   const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+void launch_planes_t(int kr, int ch, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
+                     const GridOut &go, const TileGeom &g, const Scratch &sc, const FusedIn &fi,
+                     cudaStream_t st) {
     if (kr == 0)
-        launch_planes_kr<NW, 0>(bm, bp, bfs, po, go, g, sc, st);
+        launch_planes_kr<NW, 0>(ch, bm, bp, bfs, po, go, g, sc, fi, st);
     else if (kr == 1)
-        launch_planes_kr<NW, 1>(bm, bp, bfs, po, go, g, sc, st);
+        launch_planes_kr<NW, 1>(ch, bm, bp, bfs, po, go, g, sc, fi, st);
     else
-        launch_planes_kr<NW, 2>(bm, bp, bfs, po, go, g, sc, st);
+        launch_planes_kr<NW, 2>(ch, bm, bp, bfs, po, go, g, sc, fi, st);
 }
-
 
 }  // namespace hogb200

@@ -3,11 +3,12 @@
 
 namespace hogb200 {
 
-void launch_planes_d(int nw, int kr, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
-                     const GridOut &go, const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+void launch_planes_d(int nw, int kr, int ch, const int8_t *bm, int64_t bp, int64_t bfs,
+                     const PlaneOut &po, const GridOut &go, const TileGeom &g, const Scratch &sc,
+                     const FusedIn &fi, cudaStream_t st) {
     switch (nw) {
-        case 8: launch_planes_t<8>(kr, bm, bp, bfs, po, go, g, sc, st); break;
-        case 9: launch_planes_t<9>(kr, bm, bp, bfs, po, go, g, sc, st); break;
+        case 8: launch_planes_t<8>(kr, ch, bm, bp, bfs, po, go, g, sc, fi, st); break;
+        case 9: launch_planes_t<9>(kr, ch, bm, bp, bfs, po, go, g, sc, fi, st); break;
         default: break;
     }
 }

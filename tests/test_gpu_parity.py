@@ -284,3 +284,21 @@ def test_lattice_scores_vs_oracle(stride, norm):
         planes = O.integral_stack(O.gradient_map(frames[i], lut), 8)
         ref = O.scan_scores(planes, g, stride, w, 0.25)
         np.testing.assert_allclose(p.scores[i].cpu().numpy(), ref, rtol=1e-9, atol=score_tol(w))
+
+
+@pytest.mark.parametrize("key", ["c2", "c4", "c3"])
+def test_fused_lookback_variant_matches(monkeypatch, key):
+    # opt-in fused kernel (binning + decoupled look-back inside k_planes) is
+    # bit-identical to the three-kernel path
+    cfg = synth.CONFIGS[key]
+    frames = synth.make_batch(cfg, 3, 3)
+    outs = []
+    for fused in ("0", "1"):
+        monkeypatch.setenv("HOGB200_FUSED", fused)
+        p = H.HogPipeline(3, cfg.channels, cfg.height, cfg.width, cfg.bins, stride=cfg.stride)
+        p.upload(frames)
+        p.run()
+        torch.cuda.synchronize()
+        outs.append((p.binmap_view().clone(), p.planes_view().clone(), p.grid.clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
