@@ -45,7 +45,19 @@ int check_launch(const char *what) {
 }
 
 
-TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int cell, bool v8ok) {
+static int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return (e && *e) ? atoi(e) : dflt;
+}
+
+// k_planes shared memory per CTA must allow two resident CTAs per SM
+constexpr int K2_SMEM_BUDGET = 113 * 1024;
+
+// tma: k_planes stages plane rows in shared memory and writes them with TMA
+// bulk stores (needs 32-B aligned plane rows, po.vec); one extra store warp,
+// so at most 7 compute warps (strips) per CTA.
+TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int cell, bool v8ok,
+                   bool tma) {
     TileGeom g{};
     g.n = n; g.h = h; g.w = w; g.bins = bins;
     g.NWB = (bins + 3) / 4;
@@ -65,7 +77,14 @@ TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int ce
         g.halo = 0;
     }
     g.ns = (w + g.Ws - 1) / g.Ws;
-    g.NWARP = g.ns < 8 ? g.ns : 8;
+    // Opt-in (HOGB200_TMA=1).  Measured on B200 (c2, 128 frames): 334 us vs 281 us
+    // with per-thread 16-B stores -- the plane kernel is issue/latency-bound, not
+    // store-bound, and staging adds shared-memory traffic and 9% instructions
+    // (profiles/r1_tma_store_ab.md).  Pure stores do reach 7.2 TB/s this way
+    // (tools/probe_tma_store.cu) against 5.5 TB/s for st.global.
+    tma = tma && env_int("HOGB200_TMA", 0) != 0;
+    const int maxw = tma ? 7 : 8;
+    g.NWARP = g.ns < maxw ? g.ns : maxw;
     g.nss = (g.ns + g.NWARP - 1) / g.NWARP;
     g.nc1 = (w + CHUNK - 1) / CHUNK;
     g.Wc = g.nc1 * CHUNK;
@@ -82,6 +101,31 @@ TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int ce
     g.nb1 = (h + R - 1) / R;
     g.nb2 = h / R + 1;
     g.Lrows = R + g.halo;
+    g.TMA = tma ? 1 : 0;
+    if (tma) {
+        // widest CTA (fewest super-strips) whose staging ring of >= 3 rows (else 2)
+        // fits the two-CTAs-per-SM budget
+        const int kr = fused ? cell / stride : 0;
+        const int ring_env = env_int("HOGB200_RING", 0), nw_env = env_int("HOGB200_NWARP", 0);
+        bool done = false;
+        for (int minring = 3; minring >= 2 && !done; --minring) {
+            for (int nw = (nw_env > 0 && nw_env < g.NWARP) ? nw_env : g.NWARP; nw >= 1 && !done; --nw) {
+                TileGeom t = g;
+                t.nss = (g.ns + nw - 1) / nw;
+                t.NWARP = (g.ns + t.nss - 1) / t.nss;
+                t.SEGW = (int)round_up((int64_t)t.NWARP * t.Ws + 8, 8);
+                for (int ring = ring_env > 0 ? ring_env : 4; ring >= minring; --ring) {
+                    t.RING = ring;
+                    if (k2_smem_words(t, kr) * 4 <= K2_SMEM_BUDGET || ring_env > 0) {
+                        g = t;
+                        done = true;
+                        break;
+                    }
+                }
+            }
+        }
+        if (!done) g.TMA = 0;  // per-thread stores
+    }
     return g;
 }
 
@@ -143,7 +187,7 @@ int integral_impl(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w
         launch_generic_integral(bm, bp, bfs, po, n, h, w, bins, st);
         return check_launch("integral (generic)");
     }
-    TileGeom g = make_geom(n, h, w, bins, false, 0, 0, v8_ok(po, bm, bp, bfs));
+    TileGeom g = make_geom(n, h, w, bins, false, 0, 0, v8_ok(po, bm, bp, bfs), po.vec != 0);
     Scratch sc{};
     size_t need = carve(g, nullptr, nullptr);
     if (scratch == nullptr || sbytes < need)
@@ -180,7 +224,7 @@ int hog_grad_bin(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
     if (c != 1 && c != 3) return fail(HOG_EINVAL, "channels must be 1 or 3, got %d", c);
     if ((e = check_pitch4(img, ip, w, "image")) || (e = check_pitch4(bm, bp, w, "binmap"))) return e;
     if (!img || !lut || !bm) return fail(HOG_EINVAL, "null buffer");
-    TileGeom g = make_geom(n, h, w, bins, false, 0, 0, false);
+    TileGeom g = make_geom(n, h, w, bins, false, 0, 0, false, false);
     Scratch sc{};
     launch_grad_bin(1, c, false, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, (cudaStream_t)stream);
     return check_launch("hog_grad_bin");
@@ -191,10 +235,12 @@ size_t hog_scratch_bytes(int n, int h, int w, int bins, int stride, int cell) {
     bool fused = stride > 0 && cell > 0;
     size_t m = 0;
     for (int v8 = 0; v8 < 2; ++v8) {
-        size_t a = carve(make_geom(n, h, w, bins, fused, stride, cell, v8), nullptr, nullptr);
-        size_t b = carve(make_geom(n, h, w, bins, false, 0, 0, v8), nullptr, nullptr);
-        m = a > m ? a : m;
-        m = b > m ? b : m;
+        for (int tma = 0; tma < 2; ++tma) {
+            size_t a = carve(make_geom(n, h, w, bins, fused, stride, cell, v8, tma), nullptr, nullptr);
+            size_t b = carve(make_geom(n, h, w, bins, false, 0, 0, v8, tma), nullptr, nullptr);
+            m = a > m ? a : m;
+            m = b > m ? b : m;
+        }
     }
     return m;
 }
@@ -241,7 +287,11 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
     }
     cudaStream_t st = (cudaStream_t)stream;
     PlaneOut po = make_po(pl, pp, pns, pfs, w);
-    TileGeom g = make_geom(n, h, w, bins, kr > 0, stride, cell, v8_ok(po, bm, bp, bfs));
+    // the fused-binning variant (opt-in, below) keeps per-thread plane stores
+    const char *fenv = getenv("HOGB200_FUSED");
+    const bool want_fused = (stages & HOG_STAGE_ALL) == HOG_STAGE_ALL && po.vec && fenv && fenv[0] == '1';
+    TileGeom g = make_geom(n, h, w, bins, kr > 0, stride, cell, v8_ok(po, bm, bp, bfs),
+                           po.vec != 0 && !want_fused);
     Scratch sc{};
     size_t need = carve(g, nullptr, nullptr);
     if (scratch == nullptr || sbytes < need)
@@ -259,9 +309,7 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
     // k_scan_cols passes).  Measured slower on B200 (c2: 1.73 vs 1.29 ms per
     // step): binning is latency-bound and starves at the plane kernel's
     // occupancy, so the default is the three-kernel path.
-    const char *fenv = getenv("HOGB200_FUSED");
-    const bool fused = (stages & HOG_STAGE_ALL) == HOG_STAGE_ALL && g.nss == 1 && po.vec &&
-                       fenv && fenv[0] == '1';
+    const bool fused = want_fused && g.nss == 1;
     if (fused) {
         FusedIn fi{img, ip, ics, ifs, lut, sc.flags, sc.flags + (size_t)g.n * g.nb2};
         cudaMemsetAsync(sc.flags, 0, sizeof(uint32_t) * ((size_t)g.n * g.nb2 + 1), st);

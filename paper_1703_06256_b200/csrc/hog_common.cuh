@@ -43,6 +43,9 @@ struct TileGeom {
     int VC;     // plane columns per lane in k_planes (8: 256-bit stores, 4: 128-bit)
     int NWARP;  // warps (strips) per k_planes CTA
     int nss;    // super-strips: ceil(ns / NWARP)
+    int TMA;    // plane rows staged in shared memory and written by TMA bulk stores
+    int RING;   // TMA: staged plane rows in flight (ring slots)
+    int SEGW;   // TMA: staged columns per bin row = NWARP*Ws + 8 (32-B aligned front pad)
 };
 
 // Scratch arrays (device), carved from the caller's scratch buffer.
@@ -109,7 +112,7 @@ __device__ __forceinline__ void st_release_gpu(uint32_t *p, uint32_t v) {
 
 // shared-memory carve-up of one k_planes CTA (32-bit words, every array 16-B aligned)
 struct K2Smem {
-    int rowtot, Lsup, vtot, Tsup, ptop, ring, total;
+    int bar, rowtot, Lsup, vtot, Tsup, ptop, ring, stage, total;
 };
 
 __host__ __device__ inline int k2_r4(int v) { return (v + 3) & ~3; }
@@ -117,13 +120,15 @@ __host__ __device__ inline int k2_r4(int v) { return (v + 3) & ~3; }
 __host__ __device__ inline K2Smem k2_smem(const TileGeom &g, int kr) {
     const int NB = 2 * g.NW;
     K2Smem m;
-    m.rowtot = 0;                                                // [2][G][NWARP][NWp]
+    m.bar = 0;                                                   // TMA: u64 full[RING], empty[RING]
+    m.rowtot = m.bar + k2_r4(g.TMA ? 4 * g.RING : 0);            // [2][G][NWARP][NWp]
     m.Lsup = m.rowtot + k2_r4(2 * K2_G * g.NWARP * g.NWp);       // [2][Lrows][NWp]
     m.vtot = m.Lsup + k2_r4(2 * g.Lrows * g.NWp);                // [NWARP][NB]
     m.Tsup = m.vtot + k2_r4(g.NWARP * NB);                       // [2][NB]
     m.ptop = m.Tsup + k2_r4(2 * NB);                             // [NWARP][NB][32][VC]
     m.ring = m.ptop + k2_r4(g.NWARP * NB * 32 * g.VC);           // [NWARP][KR][NB][32]
-    m.total = m.ring + k2_r4(g.NWARP * kr * NB * 32);
+    m.stage = m.ring + k2_r4(g.NWARP * kr * NB * 32);             // TMA: [RING][bins][SEGW]
+    m.total = m.stage + (g.TMA ? g.RING * g.bins * g.SEGW : 0);
     return m;
 }
 
@@ -132,6 +137,60 @@ __host__ __device__ inline int k2_smem_words(const TileGeom &g, int kr) { return
 
 // ---------------------------------------------------------------------------
 // Device helpers
+
+// mbarrier + TMA bulk-store primitives (k_planes store pipeline)
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(smem_addr(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_addr(b)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+// waiter that backs off, so a spinning store warp does not take issue slots
+// from the compute warps on its scheduler
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *b, uint32_t parity) {
+    uint32_t done;
+    for (;;) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_addr(b)), "r"(parity)
+            : "memory");
+        if (done) return;
+        __nanosleep(100);
+    }
+}
+__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_addr(ssrc)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// generic-proxy shared-memory writes -> visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// barrier over the first `threads` threads of the CTA (the compute warps)
+__device__ __forceinline__ void named_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 #pragma unroll

@@ -172,11 +172,19 @@ __device__ __forceinline__ void bin_rows(const FusedIn &fi, const TileGeom &g, i
 // CH > 0: fused variant -- the CTA bins its own rows from the frame (CH
 // channels) and gets the column counts above its band by decoupled look-back
 // over the bands above (tickets keep the waits acyclic); requires nss == 1.
-template <int NW, int KR, int VC, bool VEC, int CH = 0>
+//
+// TMA: plane rows are not stored by the compute warps.  Each compute warp
+// writes its strip of row Y (all bins) into ring slot Y % RING in shared
+// memory and arrives on full[slot]; a store warp (warp NWARP, one lane)
+// waits on full[slot] and writes the slot's bin rows to HBM with one
+// cp.async.bulk per (bin, row) -- whole 32-B sectors, no LSU traffic -- then
+// releases the slot on empty[slot] once the TMA engine has read it.  The
+// compute warps synchronise among themselves with named barrier 1.
+template <int NW, int KR, int VC, bool VEC, int CH = 0, bool TMA = false>
 __global__ void __launch_bounds__(256, K2_MINB)
 k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, GridOut go,
          TileGeom g, Scratch sc, FusedIn fi) {
-    extern __shared__ uint32_t smem[];
+    extern __shared__ __align__(16) uint32_t smem[];
     constexpr int NB = 2 * NW;
     constexpr int NWB = (NB + 3) / 4;
     constexpr int G = K2_G;
@@ -198,6 +206,58 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
     uint32_t *Tsup = smem + lay.Tsup;                        // [2][NB]
     uint32_t *ptop = smem + lay.ptop + (warp * NB * 32 + lane) * VC;  // this lane's [NB][VC] (stride 32*VC)
     uint32_t *ring = smem + lay.ring + warp * KR * NB * 32 + lane;    // this lane's [KR][NB] (stride 32)
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + lay.bar);    // TMA: [RING] rows staged
+    uint64_t *empty = full + (TMA ? g.RING : 0);                      // TMA: [RING] slots read by TMA
+    uint32_t *stage = smem + lay.stage;                               // TMA: [RING][bins][SEGW]
+    auto csync = [&]() {
+        if constexpr (TMA) named_sync(1, 32 * nwarp);
+        else __syncthreads();
+    };
+    if constexpr (TMA) {
+        if (threadIdx.x == 0) {
+            for (int i = 0; i < g.RING; ++i) {
+                mbar_init(full + i, (uint32_t)nwarp);
+                mbar_init(empty + i, 1u);
+            }
+        }
+        // plane columns -7..0 of super-strip 0 (column 0 and the sector before it): zero
+        for (int i = threadIdx.x; i < g.RING * g.bins * 8; i += blockDim.x)
+            stage[(i >> 3) * g.SEGW + (i & 7)] = 0u;
+        fence_proxy_async();
+        __syncthreads();
+        if (warp == nwarp) {  // ---- store warp
+            if (lane == 0) {
+                const int Ys0 = b * g.R, Ys1 = min(Ys0 + g.R - 1, g.h);
+                int32_t *pf = po.pl + (int64_t)f * po.pfs;
+                uint32_t r = 0, slot = 0, phase = 0, prev = 0;
+                for (int ss = 0; ss < g.nss; ++ss) {
+                    const int xss = ss * nwarp * g.Ws;
+                    const int cb = ss == 0 ? -7 : xss + 1;  // first plane column copied
+                    const int last = min(xss + nwarp * g.Ws, g.w);
+                    const int ce = 1 + ((last + 7) & ~7);  // end column (exclusive), 32-B aligned
+                    const uint32_t bytes = (uint32_t)(ce - cb) * 4u;
+                    const int soff = cb - xss + 7;
+                    for (int Y = Ys0; Y <= Ys1; ++Y, ++r) {
+                        mbar_wait_sleep(full + slot, phase);
+                        const uint32_t *src = stage + slot * g.bins * g.SEGW + soff;
+                        int32_t *dst = pf + (int64_t)Y * po.pp + cb;
+                        for (int n = 0; n < g.bins; ++n)
+                            bulk_store(dst + n * po.pns, src + n * g.SEGW, bytes);
+                        bulk_commit();
+                        if (r > 0) {  // the previous row's slot has been read: release it
+                            bulk_wait_read<1>();
+                            mbar_arrive(empty + prev);
+                        }
+                        prev = slot;
+                        if (++slot == (uint32_t)g.RING) slot = 0, phase ^= 1u;
+                    }
+                }
+                bulk_wait_read<0>();
+            }
+            return;
+        }
+    }
+    uint32_t tslot = 0, tphase = 0, trow = 0;  // TMA ring position of the next stored row
 
     const int Y0 = b * g.R;
     const int Ystore = min(Y0 + g.R - 1, g.h);
@@ -227,6 +287,7 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
         const int X0 = x + 1;
         const bool st = active && own && X0 <= g.w;
         const bool lat_lane = KR && st && (x % ls) == 0 && x <= (go.ncx - 1) * ls;
+        const int soff = warp * g.Ws + VC * lane + 8;  // TMA: stage column of the lane's first value
         const int gcol = x / ls;
         const uint32_t *rdL = Lsup + (ss & 1) * g.Lrows * NWp;
         uint32_t *wrL = Lsup + ((ss & 1) ^ 1) * g.Lrows * NWp;
@@ -340,7 +401,7 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                 }
             }
         }
-        __syncthreads();
+        csync();
         if (active) {
 #pragma unroll
             for (int n = 0; n < NB; ++n) {
@@ -361,6 +422,33 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
         // plane row pointer (plane 0, the lane's first column) of the next row to store
         int32_t *prow = plf + (int64_t)Y0 * pp + X0;
         auto store_row = [&]() {
+            if constexpr (TMA) {
+                if (trow >= (uint32_t)g.RING) mbar_wait(empty + tslot, tphase ^ 1u);
+                if (st) {
+                    uint32_t *sp = stage + tslot * g.bins * g.SEGW + soff;
+#pragma unroll
+                    for (int n = 0; n < NB; ++n) {
+                        if (n < NB - 1 || !odd) {
+#pragma unroll
+                            for (int k = 0; k < VC; k += 4) {
+                                const uint4 t4 = *reinterpret_cast<const uint4 *>(ptop + n * 32 * VC + k);
+                                const uint32_t add = Lacc[n];
+                                *reinterpret_cast<uint4 *>(sp + n * g.SEGW + k) =
+                                    make_uint4(t4.x + add + half16(Q[n >> 1][k], n & 1),
+                                               t4.y + add + half16(Q[n >> 1][k + 1], n & 1),
+                                               t4.z + add + half16(Q[n >> 1][k + 2], n & 1),
+                                               t4.w + add + half16(Q[n >> 1][k + 3], n & 1));
+                            }
+                        }
+                    }
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(full + tslot);
+                ++trow;
+                if (++tslot == (uint32_t)g.RING) tslot = 0, tphase ^= 1u;
+                return;
+            }
             if (s == 0 && lane == 0) {
                 // padded column X = 0; on aligned rows also the previous row's tail
                 // padding, so that sector is written whole
@@ -452,31 +540,42 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
             ++li;
         };
 
-        if (active) {
-            store_row();
-            if (KR) lattice();
-        }
+        if (active || TMA) store_row();  // (TMA: idle warps still pass every ring slot)
+        if (active && KR) lattice();
 
         const int8_t *brow = bmf + (int64_t)Y0 * bp + x;
         const bool bin_ok = active && x < g.w;
         const int bvalid = g.w - x;  // bytes of the lane's chunk inside the frame
+        // prefetch: raw loads only, so that nothing waits on them until the
+        // group that consumes them (bytes past w are masked at use, mask_bm)
         auto load_bm = [&](int rel) -> BmWord<VC> {
             BmWord<VC> r;
             const bool ok = bin_ok && Y0 + rel < Ycomp;
             if constexpr (VC == 8) {
-                uint2 v = ok ? __ldg(reinterpret_cast<const uint2 *>(brow + (int64_t)rel * bp))
-                             : make_uint2(0xffffffffu, 0xffffffffu);
-                if (bvalid < 8) {  // bytes past w count nowhere
-                    if (bvalid < 4) v.x |= 0xffffffffu << (8 * max(bvalid, 0)), v.y = 0xffffffffu;
-                    else v.y |= 0xffffffffu << (8 * (bvalid - 4));
-                }
+                const uint2 v = ok ? __ldg(reinterpret_cast<const uint2 *>(brow + (int64_t)rel * bp))
+                                   : make_uint2(0xffffffffu, 0xffffffffu);
                 r.lo = v.x;
                 r.hi = v.y;
             } else {
-                uint32_t v = ok ? __ldg(reinterpret_cast<const uint32_t *>(brow + (int64_t)rel * bp))
-                                : 0xffffffffu;
-                if (bvalid < 4) v |= 0xffffffffu << (8 * max(bvalid, 0));
-                r.w = v;
+                r.w = ok ? __ldg(reinterpret_cast<const uint32_t *>(brow + (int64_t)rel * bp)) : 0xffffffffu;
+            }
+            return r;
+        };
+        uint32_t mlo = 0, mhi = 0;  // bytes past w count nowhere
+        if constexpr (VC == 8) {
+            if (bvalid < 8) {
+                if (bvalid < 4) mlo = 0xffffffffu << (8 * max(bvalid, 0)), mhi = 0xffffffffu;
+                else mhi = 0xffffffffu << (8 * (bvalid - 4));
+            }
+        } else {
+            if (bvalid < 4) mlo = 0xffffffffu << (8 * max(bvalid, 0));
+        }
+        auto mask_bm = [&](BmWord<VC> r) -> BmWord<VC> {
+            if constexpr (VC == 8) {
+                r.lo |= mlo;
+                r.hi |= mhi;
+            } else {
+                r.w |= mlo;
             }
             return r;
         };
@@ -501,7 +600,7 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
             if (active) {
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
-                    bw[i] = nxt[i];
+                    bw[i] = mask_bm(nxt[i]);
                     nxt[i] = load_bm(rel + G + i);  // next group in flight during this one
                 }
 #pragma unroll
@@ -526,12 +625,12 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                     }
                 }
             }
-            __syncthreads();
+            csync();
             // ---- phase B: carries, accumulate, store, lattice
+            // row-carry of (row i, word w) into this strip, one entry per lane:
+            // Lc = (carry left of this super-strip) + sum of the strip totals to the left
+            uint32_t Lsum[(NE + 31) / 32];
             if (active) {
-                // row-carry of (row i, word w) into this strip, one entry per lane:
-                // Lc = (carry left of this super-strip) + sum of the strip totals to the left
-                uint32_t Lsum[(NE + 31) / 32];
 #pragma unroll
                 for (int r = 0; r < (NE + 31) / 32; ++r) {
                     const int e = lane + 32 * r;
@@ -550,9 +649,11 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                     }
                     Lsum[r] = L;
                 }
+            }
 #pragma unroll
-                for (int i = 0; i < G; ++i) {
-                    if (Y0 + rel + i < Ycomp) {
+            for (int i = 0; i < G; ++i) {
+                if (Y0 + rel + i < Ycomp) {
+                    if (active) {
                         uint32_t hb[VC], one[VC];
 #pragma unroll
                         for (int k = 0; k < VC; ++k) {
@@ -573,32 +674,33 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                                 Q[w][k] += run;
                             }
                         }
-                        if (Y0 + rel + i + 1 <= Ystore) store_row();
-                        if (KR && --latc == 0) {
-                            latc = ls;
-                            lattice();
-                        }
+                    }
+                    if (Y0 + rel + i + 1 <= Ystore && (active || TMA)) store_row();
+                    if (active && KR && --latc == 0) {
+                        latc = ls;
+                        lattice();
                     }
                 }
             }
         }
-        __syncthreads();
+        csync();
     }
 }
 
-template <int NW, int KR, int VC, bool VEC, int CH>
+template <int NW, int KR, int VC, bool VEC, int CH, bool TMA = false>
 void launch_planes_vc(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
                       const GridOut &go, const TileGeom &g, const Scratch &sc, const FusedIn &fi,
                       cudaStream_t st) {
     const size_t smem = (size_t)k2_smem_words(g, KR) * 4;
     static size_t configured = 0;  // per instantiation
     if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(k_planes<NW, KR, VC, VEC, CH>,
+        cudaFuncSetAttribute(k_planes<NW, KR, VC, VEC, CH, TMA>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = smem;
     }
-    k_planes<NW, KR, VC, VEC, CH><<<(unsigned)((int64_t)g.n * g.nb2), 32 * g.NWARP, smem, st>>>(
-        bm, bp, bfs, po, go, g, sc, fi);
+    k_planes<NW, KR, VC, VEC, CH, TMA>
+        <<<(unsigned)((int64_t)g.n * g.nb2), 32 * (g.NWARP + (TMA ? 1 : 0)), smem, st>>>(
+            bm, bp, bfs, po, go, g, sc, fi);
 }
 
 template <int NW, int KR>
@@ -616,6 +718,12 @@ void launch_planes_kr(int ch, const int8_t *bm, int64_t bp, int64_t bfs, const P
             if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 3>(bm, bp, bfs, po, go, g, sc, fi, st);
         }
         return launch_planes_vc<NW, KR, 4, true, 3>(bm, bp, bfs, po, go, g, sc, fi, st);
+    }
+    if (g.TMA) {  // plane rows through shared memory and TMA bulk stores (requires po.vec)
+        if constexpr (NW <= 5) {
+            if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 0, true>(bm, bp, bfs, po, go, g, sc, fi, st);
+        }
+        return launch_planes_vc<NW, KR, 4, true, 0, true>(bm, bp, bfs, po, go, g, sc, fi, st);
     }
     if constexpr (NW <= 5) {
         if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 0>(bm, bp, bfs, po, go, g, sc, fi, st);

@@ -302,3 +302,29 @@ def test_fused_lookback_variant_matches(monkeypatch, key):
         outs.append((p.binmap_view().clone(), p.planes_view().clone(), p.grid.clone()))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("shape", [("c2", None), ("c4", None), ("c3", None), ("c5", (600, 2100))])
+def test_tma_store_variant_matches(monkeypatch, shape):
+    # opt-in TMA store path (plane rows staged in shared memory, written by
+    # cp.async.bulk from a store warp): bit-identical to the default path and
+    # to the oracle; the c5 crop (N_b = 18, 2100 wide) runs several super-strips
+    key, crop = shape
+    cfg = synth.CONFIGS[key]
+    h, w = crop or (cfg.height, cfg.width)
+    frames = synth.make_batch(cfg, 5, 2) if crop is None else \
+        np.ascontiguousarray(synth.make_batch(cfg, 5, 1)[:, :, :h, :w])
+    n = frames.shape[0]
+    outs = []
+    for tma in ("0", "1"):
+        monkeypatch.setenv("HOGB200_TMA", tma)
+        p = H.HogPipeline(n, cfg.channels, h, w, cfg.bins, stride=cfg.stride)
+        p.upload(frames)
+        p.run()
+        torch.cuda.synchronize()
+        outs.append((p.binmap_view().clone(), p.planes_view().clone(), p.grid.clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    lut = O.build_lut(cfg.bins)
+    ref = O.integral_stack(O.gradient_map(frames[n - 1], lut), cfg.bins)
+    assert np.array_equal(outs[1][1][n - 1].cpu().numpy().view(np.uint32), ref)
