@@ -48,6 +48,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--pyr-chunk", type=int, default=16,
+                    help="c5: frames per pyramid chunk (level buffers: ~7.8 GB of planes per frame)")
     return ap.parse_args()
 
 
@@ -391,7 +393,7 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
 
     p = H.PyramidPipeline(nf, cfg.channels, cfg.height, cfg.width, cfg.bins, stride=cfg.stride,
                           scale_step=cfg.pyramid_step, weights=weights, bias=bias,
-                          chunk=min(4, nf), device=dev)
+                          chunk=min(args.pyr_chunk, nf), device=dev)
     p.upload(frames)
     p.run()
     torch.cuda.synchronize()

@@ -395,7 +395,8 @@ int hog_resize_bilinear(const uint8_t *src, int n, int c, int h, int w, int64_t 
     g_err.clear();
     if (n < 1 || c < 1 || h < 1 || w < 1 || nh < 1 || nw < 1 || !src || !dst)
         return fail(HOG_EINVAL, "bad arguments");
-    const int64_t tot = (int64_t)n * c * nh * nw;
+    if (nh > 65535 || (int64_t)n * c > 65535)
+        return fail(HOG_EINVAL, "resize: nh (%d) and n*c (%lld) must be <= 65535", nh, (long long)n * c);
     launch_resize(src, n, c, h, w, sp, scs, sfs, nh, nw, ry, rx, dst, dp, dcs, dfs,
                   (cudaStream_t)stream);
     return check_launch("hog_resize_bilinear");

@@ -246,16 +246,15 @@ __global__ void k_window_features(const int32_t *__restrict__ grid, int ncy, int
 }
 
 // detector.py:202-221.  Explicit _rn intrinsics keep numpy's separate
-// multiply/add roundings (no FMA contraction).
-__global__ void k_resize(const uint8_t *__restrict__ src, int n, int c, int h, int w, int64_t sp,
+// multiply/add roundings (no FMA contraction).  Grid: x = output columns,
+// y = output row, z = frame * channels (no 64-bit index divisions).
+__global__ void k_resize(const uint8_t *__restrict__ src, int c, int h, int w, int64_t sp,
                          int64_t scs, int64_t sfs, int nh, int nw, double ry, double rx,
                          uint8_t *__restrict__ dst, int64_t dp, int64_t dcs, int64_t dfs) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)n * c * nh * nw) return;
-    const int j = (int)(i % nw);
-    const int r = (int)((i / nw) % nh);
-    const int ch = (int)((i / ((int64_t)nw * nh)) % c);
-    const int f = (int)(i / ((int64_t)nw * nh * c));
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nw) return;
+    const int r = blockIdx.y;
+    const int ch = blockIdx.z % c, f = blockIdx.z / c;
     double sy = __dsub_rn(__dmul_rn((double)r + 0.5, ry), 0.5);
     sy = fmin(fmax(sy, 0.0), (double)(h - 1));
     double sx = __dsub_rn(__dmul_rn((double)j + 0.5, rx), 0.5);
@@ -265,8 +264,9 @@ __global__ void k_resize(const uint8_t *__restrict__ src, int n, int c, int h, i
     const double fy = __dsub_rn(sy, (double)y0), fx = __dsub_rn(sx, (double)x0);
     const double gy = __dsub_rn(1.0, fy), gx = __dsub_rn(1.0, fx);
     const uint8_t *p = src + (int64_t)f * sfs + (int64_t)ch * scs;
-    const double a0 = (double)__ldg(p + (int64_t)y0 * sp + x0), b0 = (double)__ldg(p + (int64_t)y1 * sp + x0);
-    const double a1 = (double)__ldg(p + (int64_t)y0 * sp + x1), b1 = (double)__ldg(p + (int64_t)y1 * sp + x1);
+    const uint8_t *p0 = p + (int64_t)y0 * sp, *p1 = p + (int64_t)y1 * sp;
+    const double a0 = (double)__ldg(p0 + x0), b0 = (double)__ldg(p1 + x0);
+    const double a1 = (double)__ldg(p0 + x1), b1 = (double)__ldg(p1 + x1);
     const double r0 = __dadd_rn(__dmul_rn(a0, gy), __dmul_rn(b0, fy));
     const double r1 = __dadd_rn(__dmul_rn(a1, gy), __dmul_rn(b1, fy));
     double m = rint(__dadd_rn(__dmul_rn(r0, gx), __dmul_rn(r1, fx)));
@@ -311,6 +311,8 @@ void launch_window_features(const int32_t *grid, int n, int ncy, int ncx, int bi
 void launch_scores_lattice(const int32_t *grid, const double *den, int n, int ncy, int ncx,
                            int bins, int noy, int nox, int cells_y, int k, const double *wts,
                            double bias, double *scores, cudaStream_t st) {
+    if (den == nullptr && getenv("HOGB200_SCORES_V1") == nullptr)  // k_scores.cu (integer grid)
+        return launch_scores_rows(grid, n, ncy, ncx, bins, noy, nox, cells_y, k, wts, bias, scores, st);
     const int span = SC_COLS + 7 * k;
     const size_t smem =
         sizeof(double) * ((size_t)cells_y * bins * 8 + 2 * (size_t)bins * (span + span / 8 + 1));
@@ -330,9 +332,8 @@ void launch_scores_lattice(const int32_t *grid, const double *den, int n, int nc
 void launch_resize(const uint8_t *src, int n, int c, int h, int w, int64_t sp, int64_t scs,
                    int64_t sfs, int nh, int nw, double ry, double rx, uint8_t *dst, int64_t dp,
                    int64_t dcs, int64_t dfs, cudaStream_t st) {
-    const int64_t tot = (int64_t)n * c * nh * nw;
-    k_resize<<<blocks_for(tot, 256), 256, 0, st>>>(src, n, c, h, w, sp, scs, sfs, nh, nw, ry, rx,
-                                                   dst, dp, dcs, dfs);
+    const dim3 grid((unsigned)blocks_for(nw, 128), (unsigned)nh, (unsigned)(n * c));
+    k_resize<<<grid, 128, 0, st>>>(src, c, h, w, sp, scs, sfs, nh, nw, ry, rx, dst, dp, dcs, dfs);
 }
 
 }  // namespace hogb200

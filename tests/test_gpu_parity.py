@@ -328,3 +328,28 @@ def test_tma_store_variant_matches(monkeypatch, shape):
     lut = O.build_lut(cfg.bins)
     ref = O.integral_stack(O.gradient_map(frames[n - 1], lut), cfg.bins)
     assert np.array_equal(outs[1][1][n - 1].cpu().numpy().view(np.uint32), ref)
+
+
+@pytest.mark.parametrize("bins,stride,h,w", [(18, 8, 300, 1000), (8, 4, 203, 611), (9, 8, 129, 64)])
+def test_scores_rows_kernel(monkeypatch, bins, stride, h, w):
+    # k_scores_rows (cp.async-staged grid rows, fp64 register tiles) against the
+    # oracle's per-window dot products and against the first lattice kernel
+    rng = np.random.default_rng(bins * 1000 + h)
+    frames = synth.make_batch(synth.CONFIGS["c5"], 2, 1)[:, :, :h, :w].copy()
+    frames = np.concatenate([frames, rng.integers(0, 256, frames.shape, dtype=np.uint8)])
+    wts = rng.normal(0, 0.01, 128 * bins)
+    got = []
+    for v1 in (None, "1"):
+        if v1:
+            monkeypatch.setenv("HOGB200_SCORES_V1", v1)
+        p = H.HogPipeline(2, 1, h, w, bins, stride=stride, weights=wts, bias=-0.125)
+        p.upload(frames)
+        p.run()
+        torch.cuda.synchronize()
+        got.append(p.scores.cpu().numpy())
+    np.testing.assert_allclose(got[0], got[1], rtol=1e-12, atol=score_tol(wts))
+    g = O.Geometry(64, 128, 8, 1, 1, bins)
+    lut = O.build_lut(bins)
+    for i in range(2):
+        ref = O.scan_scores(O.integral_stack(O.gradient_map(frames[i], lut), bins), g, stride, wts, -0.125)
+        np.testing.assert_allclose(got[0][i], ref, rtol=1e-9, atol=score_tol(wts))
