@@ -48,6 +48,9 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--e2e-chunk", type=int, default=64, help="frames per H2D/compute/D2H chunk")
+    ap.add_argument("--e2e-slots", type=int, default=3, help="pipelines/streams in flight (e2e)")
+    ap.add_argument("--no-graph", action="store_true", help="e2e: launch eagerly, no CUDA graph")
     ap.add_argument("--pyr-chunk", type=int, default=16,
                     help="c5: frames per pyramid chunk (level buffers: ~7.8 GB of planes per frame)")
     return ap.parse_args()
@@ -334,7 +337,8 @@ def main():
     # end to end through the public API: pinned host frames in, result out, per step
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier)
+        e2e = run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier,
+                      args.e2e_chunk, args.e2e_slots, not args.no_graph)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -460,7 +464,8 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
     return 0
 
 
-def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier):
+def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, chunk=64, nslots=2,
+            use_graph=True):
     """Per step: H2D of every frame from pinned host memory, the pipeline, and
     D2H of the step's result, chunked over two streams so copies overlap
     compute."""
@@ -468,11 +473,11 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier):
 
     from paper_1703_06256_b200 import synth
 
-    chunk = max(1, min(nf, 64))
+    chunk = max(1, min(nf, chunk))
     nchunks = (nf + chunk - 1) // chunk
     weights, bias = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
     slots = []
-    for _ in range(min(2, nchunks)):
+    for _ in range(max(1, min(nslots, nchunks))):
         q = H.HogPipeline(chunk, cfg.channels, cfg.height, cfg.width, cfg.bins,
                           stride=cfg.stride, normalization=cfg.normalization, weights=weights,
                           bias=bias, device=dev)
@@ -480,9 +485,8 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier):
     host_in = torch.from_numpy(frames).pin_memory()
     res = slots[0][0].result()
     host_out = torch.empty((nf,) + tuple(res.shape[1:]), dtype=res.dtype).pin_memory()
-    cur = torch.cuda.current_stream()
-
     def step():
+        cur = torch.cuda.current_stream()
         for s in (st for _, st in slots):
             s.wait_stream(cur)
         for j in range(nchunks):
@@ -499,11 +503,23 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier):
     for _ in range(W):
         step()
     torch.cuda.synchronize()
+    replay = step
+    if use_graph:
+        # the whole step (H2D copies, kernels, D2H copies on their streams)
+        # as one CUDA graph: no per-chunk host launch cost inside the timed loop
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        torch.cuda.synchronize()
+        replay = g.replay
+        for _ in range(W):
+            replay()
+        torch.cuda.synchronize()
     barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
     for _ in range(K):
-        step()
+        replay()
     t1.record()
     torch.cuda.synchronize()
     ms = max_over_ranks([t0.elapsed_time(t1) / K])[0]
@@ -513,7 +529,8 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier):
             "ms_per_step": ms, "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
             "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
             "result": "cell grid" if not cfg.scored else "window scores",
-            "chunk_frames": chunk, "streams": len(slots), "matches_device_run": ok}
+            "chunk_frames": chunk, "streams": len(slots), "cuda_graph": bool(use_graph),
+            "matches_device_run": ok}
 
 
 if __name__ == "__main__":
