@@ -151,6 +151,36 @@ int hog_resize_bilinear(const uint8_t *src, int n, int c, int h, int w,
                         uint8_t *dst, int64_t dst_pitch, int64_t dst_cstride, int64_t dst_fstride,
                         hog_stream_t stream);
 
+/* Scratch bytes for hog_detect over n score maps of `windows` windows each. */
+size_t hog_detect_scratch_bytes(int n, int64_t windows);
+
+/* detector.py:145-153 (strict `score > threshold`, row-major window order)
+ * + :194-199 (box = rint(origin * scale), Python round half-to-even; w, h =
+ * int(round(window * scale)) given as ww, wh) + :261-267 (pyramid: clamp to
+ * an image of clamp_w x clamp_h when clamp_w > 0).  scores is [n][noy][nox]
+ * float64, oxs[nox] / oys[noy] the window origins.  Per frame f the first
+ * min(count[f], cap) hits are written in the reference's list order:
+ * boxes[f][k] = (x, y, w, h) int32, out_scores[f][k], out_window[f][k] =
+ * iy*nox + ix (out_window may be NULL).  count[f] is the total number of
+ * hits (a caller whose cap was too small sees count > cap). */
+int hog_detect(const double *scores, int n, int noy, int nox, double threshold,
+               const int32_t *oxs, const int32_t *oys, double scale, int ww, int wh,
+               int clamp_w, int clamp_h, int cap, int32_t *boxes, double *out_scores,
+               int64_t *out_window, int32_t *count, void *scratch, size_t scratch_bytes,
+               hog_stream_t stream);
+
+/* Scratch bytes for hog_nms over n detections. */
+size_t hog_nms_scratch_bytes(int n);
+
+/* detector.py:285-299 (nms): greedy non-maximum suppression of n boxes
+ * (x, y, w, h int32) with scores and scales (float64): candidates in order
+ * of (-score, y, x, scale) (stable), a candidate is kept iff its IoU
+ * (detector.py:272-282, float64) with every kept box is <= iou_threshold.
+ * keep[0 .. *keep_count) receives the kept input indices in that order. */
+int hog_nms(const int32_t *boxes, const double *scores, const double *scales, int n,
+            double iou_threshold, int32_t *keep, int32_t *keep_count, void *scratch,
+            size_t scratch_bytes, hog_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

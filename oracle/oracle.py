@@ -234,6 +234,52 @@ def pyramid_levels(width, height, g, scale_step):
     return levels
 
 
+# --- detections (pure Python: small cases only) ------------------------------
+
+def hits(scores, oxs, oys, threshold, scale, ww, wh, clamp=None):
+    """detector.py:140-154 (strict >, row-major) + 194-199 (int(round(o*scale)))
+    + 261-267 (pyramid clamp to clamp = (W, H)).  Returns (boxes, scores)."""
+    boxes, out = [], []
+    for iy in range(scores.shape[0]):
+        for ix in range(scores.shape[1]):
+            s = float(scores[iy, ix])
+            if s > threshold:
+                x, y, bw, bh = int(round(int(oxs[ix]) * scale)), int(round(int(oys[iy]) * scale)), ww, wh
+                if clamp is not None:
+                    x = min(max(x, 0), clamp[0] - 1)
+                    y = min(max(y, 0), clamp[1] - 1)
+                    bw = min(bw, clamp[0] - x)
+                    bh = min(bh, clamp[1] - y)
+                boxes.append((x, y, bw, bh))
+                out.append(s)
+    return np.array(boxes, dtype=np.int64).reshape(-1, 4), np.array(out, dtype=np.float64)
+
+
+def iou(a, b) -> float:
+    """detector.py:272-282."""
+    ax, ay, aw, ah = a
+    bx, by, bw, bh = b
+    ix = max(0.0, min(ax + aw, bx + bw) - max(ax, bx))
+    iy = max(0.0, min(ay + ah, by + bh) - max(ay, by))
+    inter = ix * iy
+    if inter <= 0.0:
+        return 0.0
+    return inter / (aw * ah + bw * bh - inter)
+
+
+def nms(boxes, scores, scales, iou_threshold) -> np.ndarray:
+    """detector.py:285-299: kept indices, in keep order.  sorted() is stable,
+    so equal keys keep input order, as in the reference."""
+    boxes = [tuple(int(v) for v in b) for b in np.asarray(boxes)]
+    order = sorted(range(len(boxes)),
+                   key=lambda i: (-float(scores[i]), boxes[i][1], boxes[i][0], float(scales[i])))
+    kept = []
+    for i in order:
+        if all(iou(boxes[i], boxes[k]) <= iou_threshold for k in kept):
+            kept.append(i)
+    return np.array(kept, dtype=np.int64)
+
+
 # --- whole-frame CPU baseline ---------------------------------------------
 
 def run_batch(frames: np.ndarray, lut: np.ndarray, bins: int, cell: int, ww: int, wh: int,

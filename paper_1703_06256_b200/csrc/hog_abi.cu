@@ -402,4 +402,48 @@ int hog_resize_bilinear(const uint8_t *src, int n, int c, int h, int w, int64_t 
     return check_launch("hog_resize_bilinear");
 }
 
+size_t hog_detect_scratch_bytes(int n, int64_t windows) {
+    if (n < 1 || windows < 1) return 0;
+    return det_scratch_bytes(n, windows);
+}
+
+int hog_detect(const double *scores, int n, int noy, int nox, double threshold, const int32_t *oxs,
+               const int32_t *oys, double scale, int ww, int wh, int clamp_w, int clamp_h, int cap,
+               int32_t *boxes, double *out_scores, int64_t *out_window, int32_t *count,
+               void *scratch, size_t sbytes, hog_stream_t stream) {
+    g_err.clear();
+    if (n < 1 || noy < 1 || nox < 1 || cap < 0 || !scores || !oxs || !oys || !count || !scratch)
+        return fail(HOG_EINVAL, "bad arguments");
+    if (cap > 0 && (!boxes || !out_scores)) return fail(HOG_EINVAL, "null output buffer");
+    if (n > 65535) return fail(HOG_EINVAL, "n must be <= 65535");
+    if (sbytes < det_scratch_bytes(n, (int64_t)noy * nox))
+        return fail(HOG_EINVAL, "scratch too small: need %zu bytes",
+                    det_scratch_bytes(n, (int64_t)noy * nox));
+    launch_detect_abi(scores, n, noy, nox, threshold, oxs, oys, scale, ww, wh, clamp_w, clamp_h,
+                      cap, boxes, out_scores, out_window, count, scratch, (cudaStream_t)stream);
+    return check_launch("hog_detect");
+}
+
+size_t hog_nms_scratch_bytes(int n) { return n < 1 ? 0 : nms_scratch_bytes(n); }
+
+int hog_nms(const int32_t *boxes, const double *scores, const double *scales, int n,
+            double iou_threshold, int32_t *keep, int32_t *keep_count, void *scratch, size_t sbytes,
+            hog_stream_t stream) {
+    g_err.clear();
+    if (!(iou_threshold >= 0.0 && iou_threshold <= 1.0))
+        return fail(HOG_EINVAL, "iou_threshold must be in [0, 1], got %g", iou_threshold);
+    if (n < 0 || !keep_count) return fail(HOG_EINVAL, "bad arguments");
+    if (n == 0) {
+        cudaMemsetAsync(keep_count, 0, sizeof(int32_t), (cudaStream_t)stream);
+        return check_launch("hog_nms");
+    }
+    if (!boxes || !scores || !scales || !keep || !scratch) return fail(HOG_EINVAL, "null buffer");
+    if (sbytes < nms_scratch_bytes(n))
+        return fail(HOG_EINVAL, "scratch too small: need %zu bytes", nms_scratch_bytes(n));
+    if (launch_nms(boxes, scores, scales, n, iou_threshold, keep, keep_count, scratch, sbytes,
+                   (cudaStream_t)stream) != 0)
+        return fail(HOG_ECUDA, "hog_nms: sort failed");
+    return check_launch("hog_nms");
+}
+
 }  // extern "C"

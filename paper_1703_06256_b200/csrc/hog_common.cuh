@@ -292,6 +292,16 @@ void launch_window_features(const int32_t *grid, int n, int ncy, int ncx, int bi
 void launch_scores_lattice(const int32_t *grid, const double *den, int n, int ncy, int ncx,
                            int bins, int noy, int nox, int cells_y, int k, const double *wts,
                            double bias, double *scores, cudaStream_t st);
+// k_detect.cu
+struct DetMap;
+size_t det_scratch_bytes(int n, int64_t m);
+size_t nms_scratch_bytes(int n);
+int launch_nms(const int32_t *boxes, const double *scores, const double *scales, int n, double thr,
+               int32_t *keep, int32_t *keep_count, void *scratch, size_t sbytes, cudaStream_t st);
+void launch_detect_abi(const double *scores, int n, int noy, int nox, double thr, const int32_t *oxs,
+                       const int32_t *oys, double scale, int ww, int wh, int clamp_w, int clamp_h,
+                       int cap, int32_t *boxes, double *out_scores, int64_t *out_window,
+                       int32_t *count, void *scratch, cudaStream_t st);
 // k_scores.cu
 void launch_scores_rows(const int32_t *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
                         int cells_y, int k, const double *wts, double bias, double *scores,

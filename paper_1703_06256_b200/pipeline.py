@@ -207,6 +207,31 @@ class HogPipeline:
                          eps_term(g.normalization), D.ptr(self.w_dev), self.bias,
                          D.ptr(self.scores), None, s)
 
+    def detections(self, threshold: float, iou_threshold: float | None = None, scale: float = 1.0):
+        """Per-frame detection lists of the last run (needs weights): windows with
+        score > threshold in row-major order (detector.py:145-153, 194-199),
+        greedy NMS when iou_threshold is given (detector.py:285-299) -- the
+        threshold, box mapping and NMS all run on the device."""
+        from . import detections as DT
+
+        if self.scores is None:
+            raise ValueError("detections need a pipeline built with weights")
+        g = self.geometry
+        ww, wh = DT.window_box_size(g.window_w, g.window_h, scale)
+        boxes, sc, _, counts = DT.compact(self.scores, self.oxs, self.oys, threshold, scale, ww, wh)
+        out = []
+        for f in range(self.n):
+            k = int(counts[f])
+            b, s = boxes[f, :k], sc[f, :k]
+            if iou_threshold is not None and k:
+                t = D.torch()
+                keep = DT.nms_indices(b, s, t.full((k,), float(scale), dtype=t.float64,
+                                                   device=b.device), iou_threshold)
+                kt = t.as_tensor(keep, device=b.device)
+                b, s = b[kt], s[kt]
+            out.append(DT.to_detections(b.cpu().numpy(), s.cpu().numpy(), scale))
+        return out
+
     def launches_per_run(self) -> int:
         k = 3 * self.chunks  # grad_bin + carry scan + planes per chunk
         k += 0 if self.fused else 1
@@ -358,18 +383,26 @@ class PyramidPipeline:
                         for (lv, _, _, _), p in zip(self.levels, self.pipes))
         return per_chunk * ((self.n + self.chunk - 1) // self.chunk)
 
-    def detections(self, frame: int, threshold: float, window=(64, 128)):
-        """Host boxes of one frame, as pyramid_scan returns them (detector.py:252-268)."""
-        from .detector import Detection
+    def detections(self, frame: int, threshold: float, iou_threshold: float | None = None,
+                   window=(64, 128)):
+        """One frame's boxes as pyramid_scan returns them (detector.py:252-268),
+        optionally followed by greedy NMS (detector.py:285-299).  Per level the
+        hits are compacted on the device with the level's scale and clamped to
+        the original frame; NMS sorts and suppresses the concatenation there."""
+        from . import detections as DT
 
-        out = []
+        t = D.torch()
+        bl, sl, cl = [], [], []
         for (level, factor, w, h), p in zip(self.levels, self.pipes):
-            sc = self.scores[level][frame].cpu().numpy()
-            ww, wh = int(round(window[0] * factor)), int(round(window[1] * factor))
-            iy, ix = np.nonzero(sc > threshold)
-            for j, i in zip(iy.tolist(), ix.tolist()):
-                x = min(max(int(round(int(p.oxs[i]) * factor)), 0), self.w - 1)
-                y = min(max(int(round(int(p.oys[j]) * factor)), 0), self.h - 1)
-                out.append(Detection(x=x, y=y, w=min(ww, self.w - x), h=min(wh, self.h - y),
-                                     score=float(sc[j, i]), scale=factor))
-        return out
+            ww, wh = DT.window_box_size(window[0], window[1], factor)
+            boxes, sc, _, counts = DT.compact(self.scores[level][frame:frame + 1], p.oxs, p.oys,
+                                              threshold, factor, ww, wh, clamp=(self.w, self.h))
+            k = int(counts[0])
+            bl.append(boxes[0, :k])
+            sl.append(sc[0, :k])
+            cl.append(t.full((k,), float(factor), dtype=t.float64, device=boxes.device))
+        b, s, c = t.cat(bl), t.cat(sl), t.cat(cl)
+        if iou_threshold is not None and len(s):
+            kt = t.as_tensor(DT.nms_indices(b, s, c, iou_threshold), device=b.device)
+            b, s, c = b[kt], s[kt], c[kt]
+        return DT.to_detections(b.cpu().numpy(), s.cpu().numpy(), c.cpu().numpy())

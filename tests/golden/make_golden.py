@@ -159,6 +159,35 @@ def main():
     out["pyramid/score"] = np.array([d.score for d in dets])
     out["pyramid/scale"] = np.array([d.scale for d in dets])
 
+    # threshold + greedy NMS (detector.py:145-153, 285-299) on the pyramid hits
+    for thr in (0.0, 1.5):
+        hits = fh.pyramid_scan(fh.Image(pimg), model, 1.3, 4, thr)
+        out[f"pyramid_thr{thr}/boxes"] = np.array([(d.x, d.y, d.w, d.h) for d in hits],
+                                                   dtype=np.int64).reshape(-1, 4)
+        out[f"pyramid_thr{thr}/score"] = np.array([d.score for d in hits])
+        out[f"pyramid_thr{thr}/scale"] = np.array([d.scale for d in hits])
+    pos = {id(d): i for i, d in enumerate(dets)}
+    for iou_t in (0.0, 0.3, 0.5, 1.0):
+        out[f"nms/pyramid/{iou_t}"] = np.array([pos[id(d)] for d in fh.nms(dets, iou_t)],
+                                               dtype=np.int64)
+    # random integer boxes with tied scores, tied (y, x) and several scales
+    rng = np.random.default_rng(777)
+    k = 1500
+    rb = np.stack([rng.integers(0, 300, k), rng.integers(0, 200, k),
+                   rng.integers(8, 120, k), rng.integers(8, 160, k)], 1)
+    rb[k // 2:, :2] = rb[: k - k // 2, :2]  # duplicate origins: ties broken by scale
+    rs = np.round(rng.normal(0, 1, k), 1)   # many equal scores
+    rc = rng.choice([1.0, 1.2, 1.44], k)
+    rdets = [fh.Detection(int(b[0]), int(b[1]), int(b[2]), int(b[3]), float(s_), float(c))
+             for b, s_, c in zip(rb, rs, rc)]
+    out["nms/random/boxes"] = rb.astype(np.int64)
+    out["nms/random/score"] = rs
+    out["nms/random/scale"] = rc
+    rpos = {id(d): i for i, d in enumerate(rdets)}
+    for iou_t in (0.0, 0.2, 0.45, 0.8, 1.0):
+        out[f"nms/random/{iou_t}"] = np.array([rpos[id(d)] for d in fh.nms(rdets, iou_t)],
+                                              dtype=np.int64)
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
     print(f"wrote {len(out)} arrays; npz size "
           f"{os.path.getsize(os.path.join(HERE, 'golden.npz')) / 1e3:.0f} kB")

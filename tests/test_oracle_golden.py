@@ -177,3 +177,40 @@ def test_pyramid_level_loop(golden):
     assert np.array_equal(np.array(boxes), golden["pyramid/boxes"])
     assert np.array_equal(np.array(scales), golden["pyramid/scale"])
     np.testing.assert_allclose(scores, golden["pyramid/score"], rtol=0, atol=_score_tol(w, 64))
+
+
+@pytest.mark.parametrize("case", ["pyramid", "random"])
+def test_oracle_nms_golden(golden, case):
+    # pins the oracle's NMS restatement to the reference's own nms() output
+    if case == "random":
+        boxes, scores, scales = (golden["nms/random/boxes"], golden["nms/random/score"],
+                                 golden["nms/random/scale"])
+        thrs = (0.0, 0.2, 0.45, 0.8, 1.0)
+    else:
+        boxes, scores, scales = (golden["pyramid/boxes"], golden["pyramid/score"],
+                                 golden["pyramid/scale"])
+        thrs = (0.0, 0.3, 0.5, 1.0)
+    for t in thrs:
+        assert np.array_equal(O.nms(boxes, scores, scales, t), golden[f"nms/{case}/{t}"])
+
+
+def test_oracle_threshold_hits_golden(golden):
+    # threshold + box mapping + clamping of every pyramid level == the
+    # reference's pyramid_scan at a finite threshold
+    img, w = golden["pyramid/image"], golden["pyramid/weights"]
+    g = O.Geometry(16, 16, 8, 2, 1, 9)
+    lut = O.build_lut(9)
+    for thr in (0.0, 1.5):
+        bl, sl, cl = [], [], []
+        for (level, factor, lw, lh) in O.pyramid_levels(img.shape[2], img.shape[1], g, 1.3):
+            lim = img if level == 0 else O.resize_bilinear(img, lw, lh)
+            sc = O.scan_scores(O.integral_stack(O.gradient_map(lim, lut), 9), g, 4, w, -0.5)
+            oxs, oys = O.window_origins(lw, lh, g, 4)
+            b, s = O.hits(sc, oxs, oys, thr, factor, int(round(16 * factor)), int(round(16 * factor)),
+                          clamp=(img.shape[2], img.shape[1]))
+            bl.append(b)
+            sl.append(s)
+            cl.append(np.full(len(s), factor))
+        assert np.array_equal(np.concatenate(bl), golden[f"pyramid_thr{thr}/boxes"])
+        np.testing.assert_allclose(np.concatenate(sl), golden[f"pyramid_thr{thr}/score"], rtol=1e-12)
+        assert np.array_equal(np.concatenate(cl), golden[f"pyramid_thr{thr}/scale"])
