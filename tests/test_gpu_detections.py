@@ -134,3 +134,19 @@ def test_pyramid_pipeline_detections_nms():
     kept = p.detections(0, thr, iou_threshold=0.4)
     ref = O.nms(rb, rs, rc, 0.4)
     assert [(d.box, d.scale) for d in kept] == [(tuple(int(v) for v in rb[i]), rc[i]) for i in ref]
+
+
+def test_nms_api_greedy_definition():
+    rng = np.random.default_rng(3)
+    for _ in range(30):
+        dets = [H.Detection(int(rng.integers(0, 40)), int(rng.integers(0, 40)),
+                            int(rng.integers(4, 20)), int(rng.integers(4, 20)),
+                            float(rng.normal())) for _ in range(int(rng.integers(0, 20)))]
+        thr = float(rng.uniform(0, 1))
+        kept = H.nms(dets, thr)
+        for i, a in enumerate(kept):
+            for b in kept[i + 1:]:
+                assert H.iou(a.box, b.box) <= thr
+        assert [k.score for k in kept] == sorted([k.score for k in kept], reverse=True)
+        ref = O.nms([d.box for d in dets], [d.score for d in dets], [d.scale for d in dets], thr)
+        assert [id(k) for k in kept] == [id(dets[i]) for i in ref]
