@@ -151,6 +151,23 @@ int hog_resize_bilinear(const uint8_t *src, int n, int c, int h, int w,
                         uint8_t *dst, int64_t dst_pitch, int64_t dst_cstride, int64_t dst_fstride,
                         hog_stream_t stream);
 
+/* integral.py:58-87 with acc_width=16: uint16 planes [n][bins][h+1][w+1]
+ * (pl_pitch >= w+1), for frames whose pixel count w*h <= 65535 (the
+ * reference's overflow guard; larger frames are rejected with HOG_EINVAL).
+ * Half the plane bytes of hog_integral. */
+int hog_integral16(const int8_t *binmap, int n, int h, int w, int64_t bm_pitch, int64_t bm_fstride,
+                   int bins, uint16_t *planes, int64_t pl_pitch, int64_t pl_nstride,
+                   int64_t pl_fstride, hog_stream_t stream);
+
+/* integral.py:95-115 (rect_count / rect_histogram) for a batch of k
+ * half-open rectangles rects[r] = (x0, y0, x1, y1) int32 of ONE frame's
+ * planes (uint32 when elem_bytes == 4, uint16 when 2):
+ *   out[r][b] = p[b][y1][x1] + p[b][y0][x0] - p[b][y1][x0] - p[b][y0][x1]  (int64).
+ * The caller validates rectangles (0 <= x0 < x1 <= w, 0 <= y0 < y1 <= h), as
+ * integral.py:90-92 does before reading. */
+int hog_rect_histogram(const void *planes, int elem_bytes, int64_t pl_pitch, int64_t pl_nstride,
+                       int bins, const int32_t *rects, int k, int64_t *out, hog_stream_t stream);
+
 /* Scratch bytes for hog_detect over n score maps of `windows` windows each. */
 size_t hog_detect_scratch_bytes(int n, int64_t windows);
 

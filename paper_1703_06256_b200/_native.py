@@ -34,6 +34,8 @@ SIGNATURES = {
     "hog_scores_lattice": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _D, _P, _P]),
     "hog_resize_bilinear": (_I, [_P, _I, _I, _I, _I, _L, _L, _L, _I, _I, _D, _D,
                                  _P, _L, _L, _L, _P]),
+    "hog_integral16": (_I, [_P, _I, _I, _I, _L, _L, _I, _P, _L, _L, _L, _P]),
+    "hog_rect_histogram": (_I, [_P, _I, _L, _L, _I, _P, _I, _P, _P]),
     "hog_detect_scratch_bytes": (_SZ, [_I, _L]),
     "hog_detect": (_I, [_P, _I, _I, _I, _D, _P, _P, _D, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
                         _SZ, _P]),

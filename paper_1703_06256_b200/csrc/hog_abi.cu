@@ -402,6 +402,30 @@ int hog_resize_bilinear(const uint8_t *src, int n, int c, int h, int w, int64_t 
     return check_launch("hog_resize_bilinear");
 }
 
+int hog_integral16(const int8_t *bm, int n, int h, int w, int64_t bp, int64_t bfs, int bins,
+                   uint16_t *pl, int64_t pp, int64_t pns, int64_t pfs, hog_stream_t stream) {
+    g_err.clear();
+    int e;
+    if ((e = check_frames(n, h, w)) || (e = check_bins(bins))) return e;
+    if ((int64_t)w * h > 65535)
+        return fail(HOG_EINVAL, "16-bit accumulators need w*h <= 65535, got %dx%d = %lld", w, h,
+                    (long long)w * h);
+    if (pp < (int64_t)w + 1) return fail(HOG_EINVAL, "plane pitch %lld < w+1", (long long)pp);
+    if (!bm || !pl) return fail(HOG_EINVAL, "null buffer");
+    launch_integral16(bm, bp, bfs, n, h, w, bins, pl, pp, pns, pfs, (cudaStream_t)stream);
+    return check_launch("hog_integral16");
+}
+
+int hog_rect_histogram(const void *pl, int elem_bytes, int64_t pp, int64_t pns, int bins,
+                       const int32_t *rects, int k, int64_t *out, hog_stream_t stream) {
+    g_err.clear();
+    if (elem_bytes != 2 && elem_bytes != 4) return fail(HOG_EINVAL, "elem_bytes must be 2 or 4");
+    if (k < 0 || bins < 1 || (k > 0 && (!pl || !rects || !out))) return fail(HOG_EINVAL, "bad arguments");
+    if (k == 0) return HOG_OK;
+    launch_rect_hist(pl, elem_bytes, pp, pns, bins, rects, k, out, (cudaStream_t)stream);
+    return check_launch("hog_rect_histogram");
+}
+
 size_t hog_detect_scratch_bytes(int n, int64_t windows) {
     if (n < 1 || windows < 1) return 0;
     return det_scratch_bytes(n, windows);

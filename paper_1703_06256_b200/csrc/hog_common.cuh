@@ -292,6 +292,11 @@ void launch_window_features(const int32_t *grid, int n, int ncy, int ncx, int bi
 void launch_scores_lattice(const int32_t *grid, const double *den, int n, int ncy, int ncx,
                            int bins, int noy, int nox, int cells_y, int k, const double *wts,
                            double bias, double *scores, cudaStream_t st);
+// k_rect.cu
+void launch_integral16(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w, int bins,
+                       uint16_t *pl, int64_t pp, int64_t pns, int64_t pfs, cudaStream_t st);
+void launch_rect_hist(const void *pl, int elem_bytes, int64_t pp, int64_t pns, int bins,
+                      const int32_t *rects, int k, int64_t *out, cudaStream_t st);
 // k_detect.cu
 struct DetMap;
 size_t det_scratch_bytes(int n, int64_t m);

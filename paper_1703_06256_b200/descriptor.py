@@ -103,6 +103,14 @@ def normalize(values: np.ndarray, scheme: str) -> np.ndarray:
 def cell_grid_device(planes: "D.DevPlanes", cell_xs, cell_ys, cell: int, stream=None):
     """descriptor.py:176-185: (N, ncy, ncx, bins) int32 on the device."""
     t = D.torch()
+    if isinstance(planes, D.DevPlanes16):  # 16-bit stack: cells as a rectangle batch
+        from .integral import rect_histograms_device
+
+        xs, ys = np.asarray(cell_xs, dtype=np.int64), np.asarray(cell_ys, dtype=np.int64)
+        X0, Y0 = np.meshgrid(xs, ys)
+        rects = np.stack([X0, Y0, X0 + cell, Y0 + cell], -1).reshape(-1, 4)
+        h = rect_histograms_device(planes, rects, stream)
+        return h.to(t.int32).reshape(1, len(ys), len(xs), planes.bins)
     cx = t.as_tensor(np.asarray(cell_xs, dtype=np.int32), device=planes.base.device)
     cy = t.as_tensor(np.asarray(cell_ys, dtype=np.int32), device=planes.base.device)
     grid = t.empty((planes.n, len(cy), len(cx), planes.bins), dtype=t.int32,
@@ -167,10 +175,7 @@ def window_descriptor(stack: IntegralStack, origin, g: DescriptorGeometry) -> np
 
 
 def _planes_of(stack: IntegralStack):
-    if stack.device is None:
-        raise _native.NativeUnavailable("IntegralStack has no device planes; build it with "
-                                        "build_integral_stack")
-    return stack.device
+    return stack.device_planes()
 
 
 def cell_lattice(origin_xs, origin_ys, g: DescriptorGeometry):

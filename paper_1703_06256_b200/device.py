@@ -155,6 +155,56 @@ def alloc_planes(n, bins, h, w, device=None) -> DevPlanes:
     return DevPlanes(base, n, bins, h, w, pitch)
 
 
+@dataclass
+class DevPlanes16:
+    """uint16 planes (N, bins, H+1, pitch), pitch = round_up(W+1, 8) (acc_width=16)."""
+
+    data: object
+    n: int
+    bins: int
+    h: int
+    w: int
+
+    @property
+    def pitch(self) -> int:
+        return self.data.shape[-1]
+
+    @property
+    def nstride(self) -> int:
+        return (self.h + 1) * self.pitch
+
+    @property
+    def fstride(self) -> int:
+        return self.bins * self.nstride
+
+    @property
+    def ptr(self) -> int:
+        return ptr(self.data)
+
+    def view(self):
+        return self.data[..., : self.w + 1]
+
+
+def alloc_planes16(n, bins, h, w, device=None) -> DevPlanes16:
+    t = require_cuda()
+    data = t.empty((n, bins, h + 1, round_up(w + 1, 8)), dtype=t.uint16, device=device or "cuda")
+    return DevPlanes16(data, n, bins, h, w)
+
+
+def upload_planes(planes: np.ndarray, device=None):
+    """A host (bins, H+1, W+1) uint32/uint16 stack -> device planes of the same width."""
+    t = require_cuda()
+    a = np.asarray(planes)
+    bins, h1, w1 = a.shape
+    if a.dtype == np.uint16:
+        out = alloc_planes16(1, bins, h1 - 1, w1 - 1, device)
+    else:
+        out = alloc_planes(1, bins, h1 - 1, w1 - 1, device)
+        a = a.astype(np.uint32).view(np.int32)
+    out.view()[0].copy_(t.from_numpy(np.ascontiguousarray(a)))
+    return out
+
+
 def scratch(n, h, w, bins, stride=0, cell=0, device=None):
     t = require_cuda()
     nbytes = int(_native.load().hog_scratch_bytes(n, h, w, bins, stride, cell))
