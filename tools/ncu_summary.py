@@ -20,11 +20,16 @@ if rows:
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
 if len(rr) > 2:
-    h, v = rr[0], rr[2]
-    for key in ["dram__bytes_read.sum", "dram__bytes_write.sum"]:
-        if key in h:
-            print(f"{key:40s} {v[h.index(key)]} {rr[1][h.index(key)]}")
-    st = [(n, v[i]) for i, n in enumerate(h) if n.startswith("smsp__pcsamp_warps_issue_stalled") and not n.endswith("not_issued")]
-    st = sorted(((n.replace("smsp__pcsamp_warps_issue_stalled_", ""), float(x.replace(",", "") or 0)) for n, x in st), key=lambda t: -t[1])
-    tot = sum(x for _, x in st) or 1
-    print("stalls:", ", ".join(f"{n} {100 * x / tot:.1f}%" for n, x in st[:8]))
+    h = rr[0]
+    ik = h.index("Kernel Name")
+    for v in rr[2:]:
+        print(f"== {v[ik][:70]}")
+        for key in ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"]:
+            if key in h:
+                print(f"   {key:40s} {v[h.index(key)]} {rr[1][h.index(key)]}")
+        st = [(n, v[i]) for i, n in enumerate(h)
+              if n.startswith("smsp__pcsamp_warps_issue_stalled") and not n.endswith("not_issued")]
+        st = sorted(((n.replace("smsp__pcsamp_warps_issue_stalled_", ""), float(x.replace(",", "") or 0))
+                     for n, x in st), key=lambda t: -t[1])
+        tot = sum(x for _, x in st) or 1
+        print("   stalls:", ", ".join(f"{n} {100 * x / tot:.1f}%" for n, x in st[:8]))
