@@ -83,7 +83,7 @@ TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int ce
     // (profiles/r1_tma_store_ab.md).  Pure stores do reach 7.2 TB/s this way
     // (tools/probe_tma_store.cu) against 5.5 TB/s for st.global.
     tma = tma && env_int("HOGB200_TMA", 0) != 0;
-    const int maxw = tma ? 7 : 8;
+    const int maxw = k2_maxt(g.NW, g.VC) / 32 - (tma ? 1 : 0);
     g.NWARP = g.ns < maxw ? g.ns : maxw;
     g.nss = (g.ns + g.NWARP - 1) / g.NWARP;
     g.nc1 = (w + CHUNK - 1) / CHUNK;

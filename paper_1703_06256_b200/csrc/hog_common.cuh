@@ -90,6 +90,14 @@ struct GridOut {
 
 constexpr int K2_G = 4;  // rows per phase-A/phase-B group
 
+// Max threads per k_planes CTA (NWARP compute warps [+ the TMA store warp]),
+// i.e. the register budget at two CTAs per SM: 256 threads -> 128 registers,
+// 192 -> 168.  Measured on B200 (tools/ab_lib.sh, K2_MAXT variants): the
+// 8-column-per-lane and >= 10-bin variants spill at 128 registers and run
+// 4-29 % faster with 168 (c3, c4, c5); the c2 variant (4 columns, 8 bins) is
+// 4 % faster at 128.
+__host__ __device__ constexpr int k2_maxt(int nw, int vc) { return (vc == 8 || nw >= 5) ? 192 : 256; }
+
 // Inputs of the fused plane kernel (binning inside k_planes, band carries by
 // decoupled look-back instead of k_grad_bin counts + k_scan_cols).
 struct FusedIn {

@@ -169,6 +169,7 @@ __device__ __forceinline__ void bin_rows(const FusedIn &fi, const TileGeom &g, i
 #ifndef K2_MINB
 #define K2_MINB 2
 #endif
+
 // CH > 0: fused variant -- the CTA bins its own rows from the frame (CH
 // channels) and gets the column counts above its band by decoupled look-back
 // over the bands above (tickets keep the waits acyclic); requires nss == 1.
@@ -181,7 +182,7 @@ __device__ __forceinline__ void bin_rows(const FusedIn &fi, const TileGeom &g, i
 // releases the slot on empty[slot] once the TMA engine has read it.  The
 // compute warps synchronise among themselves with named barrier 1.
 template <int NW, int KR, int VC, bool VEC, int CH = 0, bool TMA = false>
-__global__ void __launch_bounds__(256, K2_MINB)
+__global__ void __launch_bounds__(k2_maxt(NW, VC), K2_MINB)
 k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, GridOut go,
          TileGeom g, Scratch sc, FusedIn fi) {
     extern __shared__ __align__(16) uint32_t smem[];

@@ -246,32 +246,61 @@ __global__ void k_window_features(const int32_t *__restrict__ grid, int ncy, int
 }
 
 // detector.py:202-221.  Explicit _rn intrinsics keep numpy's separate
-// multiply/add roundings (no FMA contraction).  Grid: x = output columns,
-// y = output row, z = frame * channels (no 64-bit index divisions).
-__global__ void k_resize(const uint8_t *__restrict__ src, int c, int h, int w, int64_t sp,
-                         int64_t scs, int64_t sfs, int nh, int nw, double ry, double rx,
-                         uint8_t *__restrict__ dst, int64_t dp, int64_t dcs, int64_t dfs) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= nw) return;
-    const int r = blockIdx.y;
+// multiply/add roundings (no FMA contraction).  A thread owns RZ_C adjacent
+// output columns (their source columns and weights are computed once) and
+// walks RZ_R output rows; one 4-byte store per row when the row is aligned.
+// Grid: x = column groups, y = row groups, z = frame * channels.
+constexpr int RZ_C = 4, RZ_R = 16;
+
+__global__ void __launch_bounds__(128)
+k_resize(const uint8_t *__restrict__ src, int c, int h, int w, int64_t sp, int64_t scs, int64_t sfs,
+         int nh, int nw, double ry, double rx, uint8_t *__restrict__ dst, int64_t dp, int64_t dcs,
+         int64_t dfs) {
+    const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * RZ_C;
+    if (j0 >= nw) return;
     const int ch = blockIdx.z % c, f = blockIdx.z / c;
-    double sy = __dsub_rn(__dmul_rn((double)r + 0.5, ry), 0.5);
-    sy = fmin(fmax(sy, 0.0), (double)(h - 1));
-    double sx = __dsub_rn(__dmul_rn((double)j + 0.5, rx), 0.5);
-    sx = fmin(fmax(sx, 0.0), (double)(w - 1));
-    const int y0 = (int)floor(sy), x0 = (int)floor(sx);
-    const int y1 = min(y0 + 1, h - 1), x1 = min(x0 + 1, w - 1);
-    const double fy = __dsub_rn(sy, (double)y0), fx = __dsub_rn(sx, (double)x0);
-    const double gy = __dsub_rn(1.0, fy), gx = __dsub_rn(1.0, fx);
+    int x0[RZ_C], x1[RZ_C];
+    double fx[RZ_C], gx[RZ_C];
+#pragma unroll
+    for (int q = 0; q < RZ_C; ++q) {
+        const int j = min(j0 + q, nw - 1);
+        double sx = __dsub_rn(__dmul_rn((double)j + 0.5, rx), 0.5);
+        sx = fmin(fmax(sx, 0.0), (double)(w - 1));
+        x0[q] = (int)floor(sx);
+        x1[q] = min(x0[q] + 1, w - 1);
+        fx[q] = __dsub_rn(sx, (double)x0[q]);
+        gx[q] = __dsub_rn(1.0, fx[q]);
+    }
     const uint8_t *p = src + (int64_t)f * sfs + (int64_t)ch * scs;
-    const uint8_t *p0 = p + (int64_t)y0 * sp, *p1 = p + (int64_t)y1 * sp;
-    const double a0 = (double)__ldg(p0 + x0), b0 = (double)__ldg(p1 + x0);
-    const double a1 = (double)__ldg(p0 + x1), b1 = (double)__ldg(p1 + x1);
-    const double r0 = __dadd_rn(__dmul_rn(a0, gy), __dmul_rn(b0, fy));
-    const double r1 = __dadd_rn(__dmul_rn(a1, gy), __dmul_rn(b1, fy));
-    double m = rint(__dadd_rn(__dmul_rn(r0, gx), __dmul_rn(r1, fx)));
-    m = fmin(fmax(m, 0.0), 255.0);
-    dst[(int64_t)f * dfs + (int64_t)ch * dcs + (int64_t)r * dp + j] = (uint8_t)m;
+    uint8_t *d = dst + (int64_t)f * dfs + (int64_t)ch * dcs + j0;
+    const bool full = j0 + RZ_C <= nw && (((uintptr_t)d | (uintptr_t)dp) & 3) == 0;
+    const int r1 = min(nh, (int)(blockIdx.y + 1) * RZ_R);
+    for (int r = blockIdx.y * RZ_R; r < r1; ++r) {
+        double sy = __dsub_rn(__dmul_rn((double)r + 0.5, ry), 0.5);
+        sy = fmin(fmax(sy, 0.0), (double)(h - 1));
+        const int y0 = (int)floor(sy), y1 = min(y0 + 1, h - 1);
+        const double fy = __dsub_rn(sy, (double)y0), gy = __dsub_rn(1.0, fy);
+        const uint8_t *p0 = p + (int64_t)y0 * sp, *p1 = p + (int64_t)y1 * sp;
+        uint32_t word = 0;
+#pragma unroll
+        for (int q = 0; q < RZ_C; ++q) {
+            const double a0 = (double)__ldg(p0 + x0[q]), b0 = (double)__ldg(p1 + x0[q]);
+            const double a1 = (double)__ldg(p0 + x1[q]), b1 = (double)__ldg(p1 + x1[q]);
+            const double r0 = __dadd_rn(__dmul_rn(a0, gy), __dmul_rn(b0, fy));
+            const double rr1 = __dadd_rn(__dmul_rn(a1, gy), __dmul_rn(b1, fy));
+            double m = rint(__dadd_rn(__dmul_rn(r0, gx[q]), __dmul_rn(rr1, fx[q])));
+            m = fmin(fmax(m, 0.0), 255.0);
+            word |= (uint32_t)m << (8 * q);
+        }
+        uint8_t *dr = d + (int64_t)r * dp;
+        if (full) {
+            *reinterpret_cast<uint32_t *>(dr) = word;
+        } else {
+#pragma unroll
+            for (int q = 0; q < RZ_C; ++q)
+                if (j0 + q < nw) dr[q] = (uint8_t)(word >> (8 * q));
+        }
+    }
 }
 
 // ---- launchers ------------------------------------------------------------
@@ -332,7 +361,8 @@ void launch_scores_lattice(const int32_t *grid, const double *den, int n, int nc
 void launch_resize(const uint8_t *src, int n, int c, int h, int w, int64_t sp, int64_t scs,
                    int64_t sfs, int nh, int nw, double ry, double rx, uint8_t *dst, int64_t dp,
                    int64_t dcs, int64_t dfs, cudaStream_t st) {
-    const dim3 grid((unsigned)blocks_for(nw, 128), (unsigned)nh, (unsigned)(n * c));
+    const dim3 grid((unsigned)blocks_for(nw, 128 * RZ_C), (unsigned)((nh + RZ_R - 1) / RZ_R),
+                    (unsigned)(n * c));
     k_resize<<<grid, 128, 0, st>>>(src, c, h, w, sp, scs, sfs, nh, nw, ry, rx, dst, dp, dcs, dfs);
 }
 

@@ -1,14 +1,14 @@
 #!/bin/bash
 # Build an experimental copy of libhogb200.so with extra nvcc flags for the
-# plane-kernel units only: tools/build_variant.sh <name> <flags...>
+# plane-kernel units and the ABI/geometry unit: tools/build_variant.sh <name> <flags...>
 # -> build/libhog_<name>.so (select with HOGB200_LIB=...)
 set -e
 name=$1; shift
 cd "$(dirname "$0")/.."
 mkdir -p build/var_$name
 objs=""
-for u in hog_abi k_bin k_window k_scores; do objs="$objs build/obj/$u.o"; done
-for u in k_planes_a k_planes_b k_planes_c k_planes_d; do
+for u in k_bin k_window k_scores k_detect k_rect; do objs="$objs build/obj/$u.o"; done
+for u in hog_abi k_planes_a k_planes_b k_planes_c k_planes_d; do
   nvcc -O3 -lineinfo -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC "$@" \
        -c -o build/var_$name/$u.o paper_1703_06256_b200/csrc/$u.cu &
   objs="$objs build/var_$name/$u.o"
