@@ -63,8 +63,13 @@ TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int ce
     g.NWB = (bins + 3) / 4;
     g.NW = (bins + 1) / 2;
     g.NWp = (int)round_up(g.NW, 4);
-    // 8 columns per lane only when every lattice column starts a lane chunk
-    g.VC = (v8ok && g.NW <= 5 && (!fused || stride % 8 == 0)) ? 8 : 4;
+    // 8 columns per lane only when every lattice column starts a lane chunk.
+    // Measured on B200 (HOGB200_VC A/B): 8 columns win for <= 8 bins on big
+    // batches (c4 planes 1.45 vs 1.55 ms); 4 columns win for 9-10 bins (c3:
+    // 1.01 vs 1.17 ms) and for single small frames (c1: 20 vs 29 us).
+    const bool big = (int64_t)n * h * w >= ((int64_t)64 << 20);
+    g.VC = (v8ok && g.NW <= 4 && big && (!fused || stride % 8 == 0) &&
+            env_int("HOGB200_VC", 8) == 8) ? 8 : 4;
     const int span = 32 * g.VC;
     if (fused) {
         int a = 8, b = stride;
