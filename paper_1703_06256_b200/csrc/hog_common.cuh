@@ -211,6 +211,16 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 
 __device__ __forceinline__ uint32_t byte_of(uint32_t v, int k) { return (v >> (8 * k)) & 0xffu; }
 
+// a << s with PTX shl semantics: shift amounts >= 32 (including "negative"
+// ones, which are huge unsigned) give 0.  One-hot packing without compares:
+// bin v lands in word w at bit offset 8v - 32w (u8x4) or 16v - 32w (u16x2)
+// exactly when that offset is in [0, 32); NO_BIN (0xFF) lands nowhere.
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t a, uint32_t s) {
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(s));
+    return r;
+}
+
 // u8x4 word -> u16x2 word holding bytes (2h, 2h+1)
 __device__ __forceinline__ uint32_t widen_half(uint32_t v, int h) {
     return h == 0 ? __byte_perm(v, 0u, 0x4140) : __byte_perm(v, 0u, 0x4342);
@@ -230,11 +240,9 @@ template <int NWB>
 __device__ __forceinline__ void count_cols(uint32_t bins4, uint32_t (&cc)[4][NWB]) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const uint32_t v = byte_of(bins4, k);
-        const uint32_t q = v >> 2, one = 1u << ((v & 3u) << 3);
+        const uint32_t s = byte_of(bins4, k) << 3;
 #pragma unroll
-        for (int w = 0; w < NWB; ++w)
-            cc[k][w] += q == (uint32_t)w ? one : 0u;
+        for (int w = 0; w < NWB; ++w) cc[k][w] += shl_clamp(1u, s - 32u * w);
     }
 }
 

@@ -611,11 +611,9 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                     for (int w = 0; w < SW; ++w) tot[w] = 0;
 #pragma unroll
                     for (int k = 0; k < VC; ++k) {
-                        const uint32_t v = bw[i].byte(k);
-                        const uint32_t q = S8 ? v >> 2 : v >> 1;
-                        const uint32_t one = S8 ? 1u << ((v & 3u) << 3) : 1u << ((v & 1u) << 4);
+                        const uint32_t s = bw[i].byte(k) << (S8 ? 3 : 4);
 #pragma unroll
-                        for (int w = 0; w < SW; ++w) tot[w] += q == (uint32_t)w ? one : 0u;
+                        for (int w = 0; w < SW; ++w) tot[w] += shl_clamp(1u, s - 32u * w);
                     }
 #pragma unroll
                     for (int w = 0; w < SW; ++w) {
@@ -655,13 +653,9 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
             for (int i = 0; i < G; ++i) {
                 if (Y0 + rel + i < Ycomp) {
                     if (active) {
-                        uint32_t hb[VC], one[VC];
+                        uint32_t s16[VC];  // bit offset of the pixel's bin in u16x2 words
 #pragma unroll
-                        for (int k = 0; k < VC; ++k) {
-                            const uint32_t v = bw[i].byte(k);
-                            hb[k] = v >> 1;
-                            one[k] = 1u << ((v & 1u) << 4);
-                        }
+                        for (int k = 0; k < VC; ++k) s16[k] = bw[i].byte(k) << 4;
 #pragma unroll
                         for (int w = 0; w < NW; ++w) {
                             const int e = i * NW + w;
@@ -671,7 +665,7 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                             uint32_t run = S8 ? widen_half(ex[i][w >> 1], w & 1) : ex[i][w];
 #pragma unroll
                             for (int k = 0; k < VC; ++k) {
-                                run += hb[k] == (uint32_t)w ? one[k] : 0u;
+                                run += shl_clamp(1u, s16[k] - 32u * w);
                                 Q[w][k] += run;
                             }
                         }
