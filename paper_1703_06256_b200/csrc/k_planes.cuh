@@ -653,20 +653,38 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
             for (int i = 0; i < G; ++i) {
                 if (Y0 + rel + i < Ycomp) {
                     if (active) {
-                        uint32_t s16[VC];  // bit offset of the pixel's bin in u16x2 words
-#pragma unroll
-                        for (int k = 0; k < VC; ++k) s16[k] = bw[i].byte(k) << 4;
 #pragma unroll
                         for (int w = 0; w < NW; ++w) {
                             const int e = i * NW + w;
                             const uint32_t L = __shfl_sync(FULL, Lsum[e / 32], e % 32);
                             Lacc[2 * w] += L & 0xffffu;
                             Lacc[2 * w + 1] += L >> 16;
-                            uint32_t run = S8 ? widen_half(ex[i][w >> 1], w & 1) : ex[i][w];
+                        }
+                        if constexpr (S8) {
+                            // strip-row prefix in u8x4 (<= 128 per bin), widened per column
+                            uint32_t r8[SW];
+#pragma unroll
+                            for (int j = 0; j < SW; ++j) r8[j] = ex[i][j];
 #pragma unroll
                             for (int k = 0; k < VC; ++k) {
-                                run += shl_clamp(1u, s16[k] - 32u * w);
-                                Q[w][k] += run;
+                                const uint32_t s8 = bw[i].byte(k) << 3;
+#pragma unroll
+                                for (int j = 0; j < SW; ++j) r8[j] += shl_clamp(1u, s8 - 32u * j);
+#pragma unroll
+                                for (int w = 0; w < NW; ++w) Q[w][k] += widen_half(r8[w >> 1], w & 1);
+                            }
+                        } else {
+                            uint32_t s16[VC];  // bit offset of the pixel's bin in u16x2 words
+#pragma unroll
+                            for (int k = 0; k < VC; ++k) s16[k] = bw[i].byte(k) << 4;
+#pragma unroll
+                            for (int w = 0; w < NW; ++w) {
+                                uint32_t run = ex[i][w];
+#pragma unroll
+                                for (int k = 0; k < VC; ++k) {
+                                    run += shl_clamp(1u, s16[k] - 32u * w);
+                                    Q[w][k] += run;
+                                }
                             }
                         }
                     }
