@@ -50,7 +50,8 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-chunk", type=int, default=64, help="frames per H2D/compute/D2H chunk")
     ap.add_argument("--e2e-slots", type=int, default=3, help="pipelines/streams in flight (e2e)")
-    ap.add_argument("--no-graph", action="store_true", help="e2e: launch eagerly, no CUDA graph")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch the timed steps (and the e2e step) eagerly, no CUDA graph")
     ap.add_argument("--pyr-chunk", type=int, default=16,
                     help="c5: frames per pyramid chunk (level buffers: ~7.8 GB of planes per frame)")
     return ap.parse_args()
@@ -298,14 +299,27 @@ def main():
             e0.record()
             e1.record()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed_steps():
+        for i in range(K):
+            p.run(plane_events=pev[i])
+
+    launch = timed_steps
+    if not args.no_graph:
+        # the K timed steps as one CUDA graph (kernel launches and the plane
+        # kernel's events are graph nodes): no host launch gaps between steps
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            timed_steps()
+        graph.replay()  # warm replay
+        launch = graph.replay
     sampler = ClockSampler(local)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     sampler.start()
     start.record()
-    for i in range(K):
-        p.run(plane_events=pev[i])
+    launch()
     end.record()
     torch.cuda.synchronize()
     clocks = sampler.stop()
@@ -358,7 +372,7 @@ def main():
                              f"traffic per GPU per step vs 126 MB L2)",
                        "k_planes_ms_per_step": plane_ms,
                        "stages_ms_diagnostic": stages_ms,
-                       "chunks": nch,
+                       "chunks": nch, "cuda_graph": not args.no_graph,
                        "overlap": "binning of chunk j+1 runs on a second stream under the "
                                   "plane writes of chunk j",
                        "fused_grid": bool(p.fused)},

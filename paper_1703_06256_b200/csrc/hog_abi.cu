@@ -306,8 +306,16 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
                (stages & HOG_STAGE_GRID_U8) ? 1 : 0};
     if (go.u8 && cell * cell > 255)
         return fail(HOG_EINVAL, "uint8 cell grid needs cell*cell <= 255 (cell %d)", cell);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (stage_events) cudaStreamIsCapturing(st, &cap);
     auto mark = [&](int i) {
-        if (stage_events && stage_events[i]) cudaEventRecord((cudaEvent_t)stage_events[i], st);
+        if (!stage_events || !stage_events[i]) return;
+        // inside a CUDA-graph capture the record becomes an external event node,
+        // so the caller can still time the stages of every replay
+        if (cap == cudaStreamCaptureStatusActive)
+            cudaEventRecordWithFlags((cudaEvent_t)stage_events[i], st, cudaEventRecordExternal);
+        else
+            cudaEventRecord((cudaEvent_t)stage_events[i], st);
     };
     // Opt-in (HOGB200_FUSED=1): the fused plane kernel bins its own rows and
     // takes the band carries by decoupled look-back (no k_grad_bin /
