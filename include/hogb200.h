@@ -105,6 +105,31 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w,
                  void *scratch, size_t scratch_bytes, int stages, void *const *stage_events,
                  hog_stream_t stream);
 
+/* Slab mode of hog_pipeline, for one frame split into row slabs across GPUs
+ * (SURVEY §8f rank 2).  `img` points at the slab's first row inside the full
+ * frame; halo_top / halo_bot say the frame continues above / below the slab
+ * (row -1 / row h are read for the vertical gradient, and rows 0 / h-1 are
+ * binned instead of being frame-border NO_BIN).  col_base (or NULL) is
+ * int32 [n][bins][w] (frame stride base_fstride): per column, the count of
+ * each bin in all frame rows above the slab -- the exclusive prefix over the
+ * slabs above of hog_column_counts.  Plane row 0 of the output is then the
+ * frame's plane row at the slab top, so every plane row equals the
+ * single-GPU result. */
+int hog_pipeline_slab(const uint8_t *img, int n, int c, int h, int w,
+                      int64_t img_pitch, int64_t img_cstride, int64_t img_fstride,
+                      const uint8_t *lut, int bins,
+                      int8_t *binmap, int64_t bm_pitch, int64_t bm_fstride,
+                      int32_t *planes, int64_t pl_pitch, int64_t pl_nstride, int64_t pl_fstride,
+                      int cell, int stride, int ncx, int ncy, int32_t *grid,
+                      void *scratch, size_t scratch_bytes, int stages, int halo_top, int halo_bot,
+                      const int32_t *col_base, int64_t base_fstride, hog_stream_t stream);
+
+/* Per-(bin, column) counts of bin-map rows [0, rows): out is int32
+ * [n][bins][w].  A slab's own contribution to the column carries of the
+ * slabs below it (integral.py:75-79 column sums restricted to the slab). */
+int hog_column_counts(const int8_t *binmap, int n, int rows, int w, int64_t bm_pitch,
+                      int64_t bm_fstride, int bins, int32_t *out, hog_stream_t stream);
+
 /* descriptor.py:176-185 for an arbitrary (sorted) cell-origin set:
  * grid[f][j][i][b] = 4-corner count of the cell at (cell_ys[j], cell_xs[i]). */
 int hog_cell_grid(const int32_t *planes, int n, int h, int w, int bins,

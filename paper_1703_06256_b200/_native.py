@@ -27,6 +27,9 @@ SIGNATURES = {
     "hog_integral": (_I, [_P, _I, _I, _I, _L, _L, _I, _P, _L, _L, _L, _P, _SZ, _P]),
     "hog_pipeline": (_I, [_P, _I, _I, _I, _I, _L, _L, _L, _P, _I, _P, _L, _L,
                           _P, _L, _L, _L, _I, _I, _I, _I, _P, _P, _SZ, _I, _P, _P]),
+    "hog_pipeline_slab": (_I, [_P, _I, _I, _I, _I, _L, _L, _L, _P, _I, _P, _L, _L,
+                               _P, _L, _L, _L, _I, _I, _I, _I, _P, _P, _SZ, _I, _I, _I, _P, _L, _P]),
+    "hog_column_counts": (_I, [_P, _I, _I, _I, _L, _L, _I, _P, _P]),
     "hog_cell_grid": (_I, [_P, _I, _I, _I, _I, _L, _L, _L, _P, _I, _P, _I, _I, _P, _P]),
     "hog_cell_norm": (_I, [_P, _I, _I, _I, _I, _D, _P, _P]),
     "hog_window_features": (_I, [_P, _I, _I, _I, _I, _P, _I, _P, _I, _I, _I, _I, _I, _I, _D,

@@ -263,12 +263,14 @@ int hog_integral(const int8_t *bm, int n, int h, int w, int64_t bp, int64_t bfs,
                          (cudaStream_t)stream);
 }
 
-int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int64_t ics,
-                 int64_t ifs, const uint8_t *lut, int bins, int8_t *bm, int64_t bp, int64_t bfs,
-                 int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, int cell, int stride, int ncx,
-                 int ncy, int32_t *grid, void *scratch, size_t sbytes, int stages,
-                 void *const *stage_events, hog_stream_t stream) {
-    g_err.clear();
+}  // extern "C"
+
+static int pipeline_impl(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int64_t ics,
+                         int64_t ifs, const uint8_t *lut, int bins, int8_t *bm, int64_t bp,
+                         int64_t bfs, int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, int cell,
+                         int stride, int ncx, int ncy, int32_t *grid, void *scratch, size_t sbytes,
+                         int stages, void *const *stage_events, int halo_top, int halo_bot,
+                         const int32_t *col_base, int64_t base_fs, hog_stream_t stream) {
     if ((stages & HOG_STAGE_ALL) == 0) stages |= HOG_STAGE_ALL;
     int e;
     if ((e = check_frames(n, h, w)) || (e = check_bins(bins))) return e;
@@ -297,11 +299,15 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
     const bool want_fused = (stages & HOG_STAGE_ALL) == HOG_STAGE_ALL && po.vec && fenv && fenv[0] == '1';
     TileGeom g = make_geom(n, h, w, bins, kr > 0, stride, cell, v8_ok(po, bm, bp, bfs),
                            po.vec != 0 && !want_fused);
+    g.ht = halo_top ? 1 : 0;
+    g.hb = halo_bot ? 1 : 0;
     Scratch sc{};
     size_t need = carve(g, nullptr, nullptr);
     if (scratch == nullptr || sbytes < need)
         return fail(HOG_EINVAL, "scratch too small: need %zu bytes, got %zu", need, sbytes);
     carve(g, scratch, &sc);
+    sc.base = col_base;
+    sc.base_fs = base_fs;
     GridOut go{grid, kr ? stride : 4, kr ? cell : 4, kr ? ncx : 1, kr ? ncy : 1,
                (stages & HOG_STAGE_GRID_U8) ? 1 : 0};
     if (go.u8 && cell * cell > 255)
@@ -322,7 +328,7 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
     // k_scan_cols passes).  Measured slower on B200 (c2: 1.73 vs 1.29 ms per
     // step): binning is latency-bound and starves at the plane kernel's
     // occupancy, so the default is the three-kernel path.
-    const bool fused = want_fused && g.nss == 1;
+    const bool fused = want_fused && g.nss == 1 && !halo_top && !halo_bot && !col_base;
     if (fused) {
         FusedIn fi{img, ip, ics, ifs, lut, sc.flags, sc.flags + (size_t)g.n * g.nb2};
         cudaMemsetAsync(sc.flags, 0, sizeof(uint32_t) * ((size_t)g.n * g.nb2 + 1), st);
@@ -343,6 +349,40 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
         mark(3);
     }
     return check_launch("hog_pipeline");
+}
+
+extern "C" {
+
+int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int64_t ics,
+                 int64_t ifs, const uint8_t *lut, int bins, int8_t *bm, int64_t bp, int64_t bfs,
+                 int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, int cell, int stride, int ncx,
+                 int ncy, int32_t *grid, void *scratch, size_t sbytes, int stages,
+                 void *const *stage_events, hog_stream_t stream) {
+    g_err.clear();
+    return pipeline_impl(img, n, c, h, w, ip, ics, ifs, lut, bins, bm, bp, bfs, pl, pp, pns, pfs,
+                         cell, stride, ncx, ncy, grid, scratch, sbytes, stages, stage_events, 0, 0,
+                         nullptr, 0, stream);
+}
+
+int hog_pipeline_slab(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int64_t ics,
+                      int64_t ifs, const uint8_t *lut, int bins, int8_t *bm, int64_t bp,
+                      int64_t bfs, int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, int cell,
+                      int stride, int ncx, int ncy, int32_t *grid, void *scratch, size_t sbytes,
+                      int stages, int halo_top, int halo_bot, const int32_t *col_base,
+                      int64_t base_fstride, hog_stream_t stream) {
+    g_err.clear();
+    return pipeline_impl(img, n, c, h, w, ip, ics, ifs, lut, bins, bm, bp, bfs, pl, pp, pns, pfs,
+                         cell, stride, ncx, ncy, grid, scratch, sbytes, stages, nullptr, halo_top,
+                         halo_bot, col_base, base_fstride, stream);
+}
+
+int hog_column_counts(const int8_t *bm, int n, int rows, int w, int64_t bp, int64_t bfs, int bins,
+                      int32_t *out, hog_stream_t stream) {
+    g_err.clear();
+    if (n < 1 || n > 65535 || rows < 0 || w < 1 || bins < 1 || bins > 64 || !bm || !out)
+        return fail(HOG_EINVAL, "bad arguments");
+    launch_column_counts(bm, bp, bfs, n, rows, w, bins, out, (cudaStream_t)stream);
+    return check_launch("hog_column_counts");
 }
 
 int hog_cell_grid(const int32_t *pl, int n, int h, int w, int bins, int64_t pp, int64_t pns,

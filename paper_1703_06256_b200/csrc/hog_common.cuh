@@ -43,6 +43,8 @@ struct TileGeom {
     int VC;     // plane columns per lane in k_planes (8: 256-bit stores, 4: 128-bit)
     int NWARP;  // warps (strips) per k_planes CTA
     int nss;    // super-strips: ceil(ns / NWARP)
+    int ht, hb; // slab mode: the frame continues above row 0 / below row h-1 (rows -1 / h are
+                // readable halo rows, and rows 0 / h-1 are binned rather than border NO_BIN)
     int TMA;    // plane rows staged in shared memory and written by TMA bulk stores
     int RING;   // TMA: staged plane rows in flight (ring slots)
     int SEGW;   // TMA: staged columns per bin row = NWARP*Ws + 8 (32-B aligned front pad)
@@ -54,6 +56,8 @@ struct Scratch {
     uint32_t *V;      // [n][nb2][Wc][NWp]  counts above each plane band, u16x2
                       //   (fused: counts above band b+1, published by band b)
     uint32_t *flags;  // [n][nb2] + 1 ticket: fused look-back state (zeroed per launch)
+    const int32_t *base;  // slab mode: [n][bins][w] column counts above plane row 0 (or null)
+    int64_t base_fs;      //   frame stride of base (elements)
 };
 
 
@@ -270,6 +274,8 @@ void launch_grad_bin(int nwb, int c, bool counts, const uint8_t *img, int64_t ip
 void launch_counts_from_bm(int nw, const int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g,
                            const Scratch &sc, cudaStream_t st);
 void launch_scan(int nw, const TileGeom &g, const Scratch &sc, cudaStream_t st);
+void launch_column_counts(const int8_t *bm, int64_t bp, int64_t bfs, int n, int rows, int w, int bins,
+                          int32_t *out, cudaStream_t st);
 // k_planes_*.cu
 void launch_planes_a(int nw, int kr, int ch, const int8_t *bm, int64_t bp, int64_t bfs,
                      const PlaneOut &po, const GridOut &go, const TileGeom &g, const Scratch &sc,

@@ -56,7 +56,8 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
     // neighbour byte outside the lane's word: left of lane 0, right of lane 31
     const int eoff = lane == 0 ? -1 : 4;
     const bool has_edge = (lane == 0 && x >= 1) || (lane == 31 && x + 4 < g.w);
-    auto rowp = [&](int y) { return col + (int64_t)min(max(y, 0), g.h - 1) * ip; };
+    // rows -1 / h exist in slab mode (g.ht / g.hb); otherwise reads clamp to the frame
+    auto rowp = [&](int y) { return col + (int64_t)min(max(y, -g.ht), g.h - 1 + g.hb) * ip; };
 
     // rows y-1 (r0), y (r1), y+1 (r2); e1/e2: edge bytes of rows y, y+1
     uint32_t r0[CH], r1[CH], r2[CH], e1[CH], e2[CH];
@@ -82,9 +83,9 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
             r3[ch] = __ldg(reinterpret_cast<const uint32_t *>(pd + ch * ics));
             e3[ch] = has_edge ? (uint32_t)__ldg(pd + ch * ics + eoff) : 0u;
         }
-        if (y + 3 < g.h) pd += ip;
+        if (y + 3 < g.h + g.hb) pd += ip;
         uint32_t bins4 = 0xffffffffu;
-        if (y > 0 && y < g.h - 1) {
+        if ((y > 0 || g.ht) && (y < g.h - 1 || g.hb)) {  // frame border rows are NO_BIN
             int bdx[4], bdy[4], bmag[4];
 #pragma unroll
             for (int ch = 0; ch < CH; ++ch) {
@@ -192,6 +193,15 @@ __global__ void k_scan_cols(TileGeom g, Scratch sc) {
     uint32_t run[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) run[w] = 0;
+    if (sc.base && x < g.w) {  // slab mode: counts above the slab's first plane row
+        const int32_t *bs = sc.base + (int64_t)f * sc.base_fs + x;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t lo = (uint32_t)bs[(int64_t)(2 * w) * g.w];
+            const uint32_t hi = 2 * w + 1 < g.bins ? (uint32_t)bs[(int64_t)(2 * w + 1) * g.w] : 0u;
+            run[w] = lo | (hi << 16);
+        }
+    }
     for (int b = 0; b < g.nb2; ++b) {
         uint32_t *vp = sc.V + (((int64_t)f * g.nb2 + b) * g.Wc + x) * g.NWp;
 #pragma unroll
@@ -235,6 +245,31 @@ void launch_grad_bin(int nwb, int c, bool counts, const uint8_t *img, int64_t ip
         case 4: grad_bin_t<4>(c, counts, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st); break;
         default: grad_bin_t<5>(c, counts, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st); break;
     }
+}
+
+// Per-(bin, column) counts of bin-map rows [0, rows): the slab's own
+// contribution to the column carries of the slabs below it (slab mode).
+__global__ void k_column_counts(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, int n,
+                                int rows, int w, int bins, int32_t *__restrict__ out) {
+    extern __shared__ int32_t ccnt[];  // [bins][blockDim.x]
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int f = blockIdx.y;
+    for (int b = 0; b < bins; ++b) ccnt[b * blockDim.x + threadIdx.x] = 0;
+    if (x < w) {
+        const int8_t *col = bm + (int64_t)f * bfs + x;
+        for (int y = 0; y < rows; ++y) {
+            const int v = col[(int64_t)y * bp];
+            if (v >= 0 && v < bins) ++ccnt[v * blockDim.x + threadIdx.x];
+        }
+        for (int b = 0; b < bins; ++b)
+            out[((int64_t)f * bins + b) * w + x] = ccnt[b * blockDim.x + threadIdx.x];
+    }
+}
+
+void launch_column_counts(const int8_t *bm, int64_t bp, int64_t bfs, int n, int rows, int w, int bins,
+                          int32_t *out, cudaStream_t st) {
+    const dim3 grid((unsigned)blocks_for(w, 128), (unsigned)n);
+    k_column_counts<<<grid, 128, sizeof(int32_t) * bins * 128, st>>>(bm, bp, bfs, n, rows, w, bins, out);
 }
 
 template <int NW>

@@ -368,7 +368,7 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
             __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) st_release_gpu(flags + b, 2u);
-        } else if (active && b > 0 && x < g.Wc) {
+        } else if (active && (b > 0 || sc.base) && x < g.Wc) {  // band 0: zero, or the slab carry
 #pragma unroll
             for (int w = 0; w < NW; ++w)
 #pragma unroll
