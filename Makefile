@@ -10,7 +10,13 @@ UNITS := hog_abi k_bin k_planes_a k_planes_b k_planes_c k_planes_d k_window k_sc
 OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(UNITS)))
 HDRS := $(CSRC)/hog_common.cuh $(CSRC)/k_planes.cuh include/hogb200.h
 
-all: $(LIB) oracle
+IOLIB := paper_1703_06256_b200/libhogio.so
+
+all: $(LIB) $(IOLIB) oracle
+
+# host wire formats (PNM decode, descriptor text): plain C++, no CUDA
+$(IOLIB): $(CSRC)/hogio.cpp include/hogio.h
+	g++ -O3 -std=c++17 -fPIC -shared -pthread -o $@ $(CSRC)/hogio.cpp
 
 $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -24,7 +30,7 @@ oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -rf $(OBJDIR) $(LIB) build_ptxas.log
+	rm -rf $(OBJDIR) $(LIB) $(IOLIB) build_ptxas.log
 	$(MAKE) -s -C oracle clean
 
 .PHONY: all oracle clean

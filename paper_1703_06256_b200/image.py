@@ -1,5 +1,5 @@
 """The input type of the hot path: an 8-bit channel-planar image
-(reference image_io.py:20-46).  PNM decoding is out of scope."""
+(reference image_io.py:20-46).  PNM decoding/encoding: image_io.py here."""
 from __future__ import annotations
 
 from dataclasses import dataclass

@@ -188,6 +188,55 @@ def main():
         out[f"nms/random/{iou_t}"] = np.array([rpos[id(d)] for d in fh.nms(rdets, iou_t)],
                                               dtype=np.int64)
 
+    # PNM wire format (image_io.py:50-122): decoded planes or the error class
+    pnm_cases = {
+        "p5": b"P5\n7 5\n255\n" + bytes(range(35)),
+        "p6": b"P6 4 3 255\n" + bytes((7 * i) % 256 for i in range(36)),
+        "p2_comments": b"P2\n# a comment\n3 2 # trailing\n255\n0 1 2\n\t 253\r254 255\n",
+        "p3": b"P3 2 2 255 1 2 3 4 5 6 7 8 9 10 11 12",
+        "p5_trailing": b"P5 2 2 255 abcdXYZ",
+        "p5_hash_after_maxval": b"P5 2 1 255#xy",
+        "p2_underscore_plus": b"P2 2 1 2_55 +7 0_0_1",
+        "p2_leading_zeros": b"P2 0002 001 0255 007 255",
+        "bad_magic": b"P4\n1 1\n255\n\x00",
+        "maxval_16bit": b"P5 1 1 65535 \x00\x00",
+        "maxval_zero": b"P5 1 1 0 \x00",
+        "truncated_raw": b"P6 2 2 255 " + bytes(11),
+        "truncated_ascii": b"P2 2 2 255 1 2 3",
+        "nonnumeric": b"P2 2 1 255 12a 3",
+        "sample_range": b"P2 1 1 255 256",
+        "negative_width": b"P5 -3 1 255 abc",
+        "empty": b"",
+        "header_only": b"P5",
+    }
+    for name, blob in pnm_cases.items():
+        out[f"pnm/{name}/bytes"] = np.frombuffer(blob, dtype=np.uint8)
+        try:
+            out[f"pnm/{name}/planes"] = fh.decode_pnm(blob).planes
+            out[f"pnm/{name}/error"] = np.array("")
+        except Exception as e:  # the reference's typed error
+            out[f"pnm/{name}/error"] = np.array(type(e).__name__)
+    # descriptor text (cli.py:124-127 _format_value)
+    from fasthog import cli as fcli
+    vals = np.array([0.0, -0.0, 0.1, 1 / 3, 1e-7, 123456789.123, 2.5e-300, 1e21, 65536.0,
+                     0.999999999, 12.0, float("inf"), -float("inf")])
+    out["fmt/values"] = vals
+    out["fmt/l2"] = np.array(" ".join(fcli._format_value(v, "l2") for v in vals))
+    ints = np.array([0, 1, 64, 4096, 33153604], dtype=np.float64)
+    out["fmt/ints"] = ints
+    out["fmt/none"] = np.array(" ".join(fcli._format_value(v, "none") for v in ints))
+
+    # `fasthog extract` text for a small image (cli.py:130-143), none and l2
+    ximg = np.random.default_rng(99).integers(0, 256, (1, 40, 52), dtype=np.uint8)
+    out["extract/image"] = ximg
+    for norm in ("none", "l2"):
+        g = fh.DescriptorGeometry(16, 24, 8, block=2, block_stride=1, bins=9, normalization=norm)
+        st = fh.build_integral_stack(fh.gradient_map(fh.Image(ximg), fh.build_lut(9)))
+        lines = []
+        for x, y, values in fh.scan_descriptors(st, g, 6):
+            lines.append(" ".join([str(x), str(y)] + [fcli._format_value(v, norm) for v in values]))
+        out[f"extract/{norm}"] = np.frombuffer(("\n".join(lines) + "\n").encode(), dtype=np.uint8)
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
     print(f"wrote {len(out)} arrays; npz size "
           f"{os.path.getsize(os.path.join(HERE, 'golden.npz')) / 1e3:.0f} kB")

@@ -54,3 +54,17 @@ def test_library_is_sm100a_only():
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
+
+
+IO_HEADER = os.path.join(ROOT, "include", "hogio.h")
+IO_LIB = os.path.join(ROOT, "paper_1703_06256_b200", "libhogio.so")
+
+
+@pytest.mark.skipif(not os.path.exists(IO_LIB), reason="libhogio.so not built")
+def test_io_library_exports_every_declared_symbol():
+    text = open(IO_HEADER).read()
+    syms = sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(hogio_[a-z_0-9]+)\s*\(",
+                                 text, re.M)))
+    assert {"hogio_pnm_decode", "hogio_decode_batch", "hogio_format_descriptors"} <= set(syms)
+    lib = ctypes.CDLL(IO_LIB)
+    assert [s for s in syms if not hasattr(lib, s)] == []
