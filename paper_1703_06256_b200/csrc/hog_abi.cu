@@ -103,7 +103,20 @@ TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int ce
     if (fused && R % stride != 0) R = (int)round_up(R, stride);
     if (R > 240) R = 240;  // u8 column counts; packed strip-local sums stay < 2^16
     g.R = R;
-    g.nb1 = (h + R - 1) / R;
+    // k_grad_bin runs R1 = R / S1 row sub-bands per warp, so its grid is several
+    // waves deep (one R-row band per warp left a 1.08-wave tail on c2)
+    g.S1 = 1;
+    const int s_env = env_int("HOGB200_SUBBANDS", 0);
+    if (s_env > 0 && R % s_env == 0) {
+        g.S1 = s_env;
+    } else if (s_env <= 0) {
+        const int64_t target = (int64_t)4 * 148 * 64;  // warps: ~4 full waves
+        while (R % (2 * g.S1) == 0 && R / (2 * g.S1) >= 16 &&
+               (int64_t)n * ((h + R / g.S1 - 1) / (R / g.S1)) * ((w + CHUNK - 1) / CHUNK) < target)
+            g.S1 *= 2;
+    }
+    g.R1 = R / g.S1;
+    g.nb1 = (h + g.R1 - 1) / g.R1;
     g.nb2 = h / R + 1;
     g.Lrows = R + g.halo;
     g.TMA = tma ? 1 : 0;
@@ -141,7 +154,7 @@ size_t carve(const TileGeom &g, void *base, Scratch *sc) {
         off += round_up((int64_t)bytes, 256);
         return o;
     };
-    size_t oC = take(sizeof(uint32_t) * (size_t)g.n * g.nb2 * g.Wc * g.NWB);
+    size_t oC = take(sizeof(uint32_t) * (size_t)g.n * (g.nb1 > g.nb2 ? g.nb1 : g.nb2) * g.Wc * g.NWB);
     size_t oV = take(sizeof(uint32_t) * (size_t)g.n * g.nb2 * g.Wc * g.NWp);
     size_t oF = take(sizeof(uint32_t) * ((size_t)g.n * g.nb2 + 1));
     if (sc && base) {

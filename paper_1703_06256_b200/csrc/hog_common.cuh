@@ -29,9 +29,10 @@ inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 struct TileGeom {
     int n, h, w, bins;
     int R;      // rows per band (multiple of the lattice step when the grid is fused)
+    int R1, S1; // k_grad_bin / k_bin_counts sub-bands: R1 = R / S1 pixel rows each
     int Ws;     // plane columns per k_planes strip (<= 128, multiple of 8)
     int ns;     // strips per frame
-    int nb1;    // pixel bands: ceil(h / R)         (k_grad_bin tiles)
+    int nb1;    // pixel sub-bands: ceil(h / R1)    (k_grad_bin tiles)
     int nb2;    // plane bands: h / R + 1            (k_planes tiles; plane rows 0..h)
     int nc1;    // 128-column chunks: ceil(w / 128)  (k_grad_bin tiles)
     int Wc;     // nc1 * 128: padded width of the per-column scratch arrays

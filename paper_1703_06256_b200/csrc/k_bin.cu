@@ -5,6 +5,11 @@
 
 namespace hogb200 {
 
+#ifndef K1_UNROLL
+#define K1_UNROLL 1
+#endif
+constexpr int K1U = K1_UNROLL;  // rows of k_grad_bin's row loop unrolled together
+
 // ---------------------------------------------------------------------------
 // K1: gradient + LUT binning (gradient.py:95-121), optionally counting bins
 // per (band, column) for k_scan_cols.  One warp = R rows x 128 columns of
@@ -28,7 +33,7 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
     const int lane = threadIdx.x & 31;
     const int x = chunk * CHUNK + 4 * lane;
     const bool inx = x < g.w;
-    const int y0 = b * g.R, y1 = min(y0 + g.R, g.h);
+    const int y0 = b * g.R1, y1 = min(y0 + g.R1, g.h);
     // lanes past the frame read (and discard) the last word of the row
     const int xl = inx ? x : ((g.w - 1) & ~3);
     const uint8_t *col = img + (int64_t)f * ifs + xl;
@@ -75,6 +80,9 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
     int8_t *bout = bm + (int64_t)f * bfs + (int64_t)y0 * bp + x;
     const uint8_t *pd = rowp(y0 + 2);  // row y+2, clamped to the last row
 
+    // unrolled so the LUT gathers of consecutive rows overlap (the kernel waits
+    // on gather latency, not on issue)
+#pragma unroll K1U
     for (int y = y0; y < y1; ++y) {
         // row y+2 in flight while row y is binned
         uint32_t r3[CH], e3[CH];
@@ -166,7 +174,7 @@ k_bin_counts(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, TileGeom g,
     const int f = (int)(wid / ((int64_t)g.nc1 * g.nb1));
     const int lane = threadIdx.x & 31;
     const int x = chunk * CHUNK + 4 * lane;
-    const int y0 = b * g.R, y1 = min(y0 + g.R, g.h);
+    const int y0 = b * g.R1, y1 = min(y0 + g.R1, g.h);
     const int8_t *bmf = bm + (int64_t)f * bfs;
     uint32_t mask = 0;  // bytes past w count nowhere
     if (x + 4 > g.w) mask = x >= g.w ? 0xffffffffu : 0xffffffffu << (8 * (g.w - x));
@@ -207,8 +215,9 @@ __global__ void k_scan_cols(TileGeom g, Scratch sc) {
 #pragma unroll
         for (int w = 0; w < NW; ++w) vp[w] = run[w];
         for (int w = NW; w < g.NWp; ++w) vp[w] = 0;
-        if (b < g.nb1) {
-            const uint32_t *cp = sc.C + (((int64_t)f * g.nb1 + b) * g.Wc + x) * NWB;
+        // plane band b covers pixel sub-bands [b*S1, (b+1)*S1)
+        for (int s = b * g.S1; s < min((b + 1) * g.S1, g.nb1); ++s) {
+            const uint32_t *cp = sc.C + (((int64_t)f * g.nb1 + s) * g.Wc + x) * NWB;
             uint32_t c8[NWB];
 #pragma unroll
             for (int w = 0; w < NWB; ++w) c8[w] = cp[w];
