@@ -433,7 +433,6 @@ int hog_window_features(const int32_t *grid, int n, int ncy, int ncx, int bins,
                     cells_x, cells_y);
     if (norm < 0 || norm > 2) return fail(HOG_EINVAL, "norm must be 0, 1 or 2");
     if (scores && !wts) return fail(HOG_EINVAL, "scores need weights");
-    const int64_t tot = (int64_t)n * noy * nox;
     launch_window_features(grid, n, ncy, ncx, bins, row_idx, noy, col_idx, nox, cells_x, cells_y,
                            block, bstride, norm, eps_term, wts, bias, scores, desc,
                            (cudaStream_t)stream);
