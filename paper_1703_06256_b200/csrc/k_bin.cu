@@ -210,17 +210,23 @@ __global__ void k_scan_cols(TileGeom g, Scratch sc) {
             run[w] = lo | (hi << 16);
         }
     }
+    // C and V never alias: read-only loads that the compiler may hoist ahead
+    // of the V stores, so several bands' loads are in flight
+    const uint32_t *__restrict__ Cf = sc.C + (int64_t)f * g.nb1 * g.Wc * NWB + (int64_t)x * NWB;
+    uint32_t *__restrict__ Vf = sc.V + (int64_t)f * g.nb2 * g.Wc * g.NWp + (int64_t)x * g.NWp;
+#pragma unroll 4
     for (int b = 0; b < g.nb2; ++b) {
-        uint32_t *vp = sc.V + (((int64_t)f * g.nb2 + b) * g.Wc + x) * g.NWp;
+        uint4 *vp = reinterpret_cast<uint4 *>(Vf + (int64_t)b * g.Wc * g.NWp);
 #pragma unroll
-        for (int w = 0; w < NW; ++w) vp[w] = run[w];
-        for (int w = NW; w < g.NWp; ++w) vp[w] = 0;
+        for (int q = 0; q < (NW + 3) / 4; ++q)  // 16-B stores; words past NW are zero padding
+            vp[q] = make_uint4(run[4 * q], 4 * q + 1 < NW ? run[4 * q + 1] : 0u,
+                               4 * q + 2 < NW ? run[4 * q + 2] : 0u, 4 * q + 3 < NW ? run[4 * q + 3] : 0u);
         // plane band b covers pixel sub-bands [b*S1, (b+1)*S1)
         for (int s = b * g.S1; s < min((b + 1) * g.S1, g.nb1); ++s) {
-            const uint32_t *cp = sc.C + (((int64_t)f * g.nb1 + s) * g.Wc + x) * NWB;
+            const uint32_t *cp = Cf + (int64_t)s * g.Wc * NWB;
             uint32_t c8[NWB];
 #pragma unroll
-            for (int w = 0; w < NWB; ++w) c8[w] = cp[w];
+            for (int w = 0; w < NWB; ++w) c8[w] = __ldg(cp + w);
 #pragma unroll
             for (int w = 0; w < NW; ++w) run[w] += widen_half(c8[w >> 1], w & 1);
         }
