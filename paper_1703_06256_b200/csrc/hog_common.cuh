@@ -214,7 +214,8 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
     return v;
 }
 
-__device__ __forceinline__ uint32_t byte_of(uint32_t v, int k) { return (v >> (8 * k)) & 0xffu; }
+// byte k of v, zero-extended: one PRMT (the shift + mask form compiles to two ops)
+__device__ __forceinline__ uint32_t byte_of(uint32_t v, int k) { return __byte_perm(v, 0u, 0x4440u | (uint32_t)k); }
 
 // a << s with PTX shl semantics: shift amounts >= 32 (including "negative"
 // ones, which are huge unsigned) give 0.  One-hot packing without compares:

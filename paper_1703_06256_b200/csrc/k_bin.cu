@@ -117,7 +117,7 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
             }
             uint32_t v[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = __ldg(lut0 + (bdx[k] * LUT_SIDE + bdy[k]));
+            for (int k = 0; k < 4; ++k) v[k] = __ldg(lut0 + (int64_t)(bdx[k] * LUT_SIDE + bdy[k]));
             bins4 = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
             bins4 = (bins4 & valid) | ~valid;
         }
