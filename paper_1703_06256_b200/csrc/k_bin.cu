@@ -27,9 +27,19 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
     constexpr int NB4 = 4 * NWB;  // bins rounded up to whole u8x4 words
     const int64_t wid = warp_id();
     if (wid >= (int64_t)g.n * g.nb1 * g.nc1) return;
-    const int chunk = (int)(wid % g.nc1);
-    const int b = (int)((wid / g.nc1) % g.nb1);
-    const int f = (int)(wid / ((int64_t)g.nc1 * g.nb1));
+    // 32-bit index math (units < 2^31 for every batch the ABI accepts in practice;
+    // 64-bit divisions are a software call)
+    int chunk, b, f;
+    if (wid < ((int64_t)1 << 31)) {
+        const uint32_t w32 = (uint32_t)wid, q = w32 / (uint32_t)g.nc1;
+        chunk = (int)(w32 - q * (uint32_t)g.nc1);
+        b = (int)(q % (uint32_t)g.nb1);
+        f = (int)(q / (uint32_t)g.nb1);
+    } else {
+        chunk = (int)(wid % g.nc1);
+        b = (int)((wid / g.nc1) % g.nb1);
+        f = (int)(wid / ((int64_t)g.nc1 * g.nb1));
+    }
     const int lane = threadIdx.x & 31;
     const int x = chunk * CHUNK + 4 * lane;
     const bool inx = x < g.w;
