@@ -68,3 +68,34 @@ def test_io_library_exports_every_declared_symbol():
     assert {"hogio_pnm_decode", "hogio_decode_batch", "hogio_format_descriptors"} <= set(syms)
     lib = ctypes.CDLL(IO_LIB)
     assert [s for s in syms if not hasattr(lib, s)] == []
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="libhogb200.so not built")
+def test_abi_rejects_bad_arguments_before_touching_the_gpu():
+    # argument checks are host code: each call returns HOG_EINVAL and sets the
+    # error text without launching anything (safe without a GPU)
+    from paper_1703_06256_b200 import _native
+
+    lib = _native.load()
+    EINVAL = _native.HOG_EINVAL
+    # frames too small / bins out of range (gradient.py:62-63, 104-105)
+    assert lib.hog_grad_bin(None, 1, 1, 2, 2, 4, 0, 0, None, 8, None, 4, 0, None) == EINVAL
+    assert b"3x3" in lib.hog_last_error()
+    assert lib.hog_grad_bin(None, 1, 1, 8, 8, 8, 0, 0, None, 65, None, 8, 0, None) == EINVAL
+    assert b"bins" in lib.hog_last_error()
+    assert lib.hog_grad_bin(None, 1, 2, 8, 8, 8, 0, 0, None, 8, None, 8, 0, None) == EINVAL
+    # fused lattice constraints
+    rc = lib.hog_pipeline(None, 1, 1, 64, 64, 64, 0, 0, None, 8, None, 64, 0, None, 72, 0, 0,
+                          8, 3, 4, 4, 1, None, 0, 0, None, None)
+    assert rc == EINVAL
+    # 16-bit accumulators: the reference's overflow guard (integral.py:66-72)
+    assert lib.hog_integral16(1, 1, 300, 300, 300, 0, 8, 1, 301, 0, 0, None) == EINVAL
+    assert b"65535" in lib.hog_last_error()
+    # NMS threshold range (detector.py:291-292)
+    assert lib.hog_nms(None, None, None, 3, 1.5, None, None, None, 0, None) == EINVAL
+    assert lib.hog_nms(None, None, None, 3, float("nan"), None, None, None, 0, None) == EINVAL
+    # resize and rectangles
+    assert lib.hog_resize_bilinear(None, 1, 1, 8, 8, 8, 0, 0, 0, 4, 1.0, 1.0, None, 4, 0, 0,
+                                   None) == EINVAL
+    assert lib.hog_rect_histogram(None, 3, 8, 8, 8, None, 1, None, None) == EINVAL
+    assert lib.hog_rect_histogram(None, 4, 8, 8, 8, None, 0, None, None) == 0  # empty batch
