@@ -182,19 +182,42 @@ void launch_rows_b(const int32_t *grid, int n, int ncy, int ncx, int bins, int n
     }
 }
 
+// Window columns per lane: the candidate (TX / K integral) that wastes the
+// fewest lanes on this width (ties to the larger TX: more reuse per grid
+// value), e.g. c4 (153 columns) -> 5 (160, 96 %), c1 (93) -> 3, 8K (953) -> 5.
+int pick_tx(int nox, int k) {
+    static const int c1[] = {5, 6, 4, 3, 2}, c2[] = {6, 4, 2};
+    const int *c = k == 1 ? c1 : c2;
+    const int nc = k == 1 ? 5 : 3;
+    int best = c[0];
+    int64_t best_pad = INT64_MAX;
+    for (int i = 0; i < nc; ++i) {
+        const int64_t cols = 32 * c[i], pad = (nox + cols - 1) / cols * cols;
+        if (pad < best_pad) best_pad = pad, best = c[i];
+    }
+    return best;
+}
+
 void launch_scores_rows(const int32_t *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
                         int cells_y, int k, const double *wts, double bias, double *scores,
                         cudaStream_t st) {
-    // 4 window columns per lane unless 2 wastes markedly fewer lanes on this width
-    const int64_t pad4 = (nox + 127) / 128 * 128, pad2 = (nox + 63) / 64 * 64;
-    const bool tx2 = pad2 * 100 < pad4 * 85;
+    const int tx = pick_tx(nox, k);
+#define SR_ARGS grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, st
     if (k == 1) {
-        if (tx2) launch_rows_b<1, 2>(grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, st);
-        else launch_rows_b<1, 4>(grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, st);
-    } else {
-        if (tx2) launch_rows_b<2, 2>(grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, st);
-        else launch_rows_b<2, 4>(grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, st);
+        switch (tx) {
+            case 2: return launch_rows_b<1, 2>(SR_ARGS);
+            case 3: return launch_rows_b<1, 3>(SR_ARGS);
+            case 4: return launch_rows_b<1, 4>(SR_ARGS);
+            case 5: return launch_rows_b<1, 5>(SR_ARGS);
+            default: return launch_rows_b<1, 6>(SR_ARGS);
+        }
     }
+    switch (tx) {
+        case 2: return launch_rows_b<2, 2>(SR_ARGS);
+        case 4: return launch_rows_b<2, 4>(SR_ARGS);
+        default: return launch_rows_b<2, 6>(SR_ARGS);
+    }
+#undef SR_ARGS
 }
 
 }  // namespace hogb200
