@@ -244,17 +244,27 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HOGB200_BENCH_SAME_GPU=1 + HOGB200_BENCH_BACKEND=gloo: plumbing check of the
+    # multi-rank path on a one-GPU box (ranks share cuda:0; nothing waits on
+    # another rank's kernels).  Real runs: one GPU per rank, NCCL.
+    if os.environ.get("HOGB200_BENCH_SAME_GPU") == "1":
+        local = 0
+    backend = os.environ.get("HOGB200_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     def max_over_ranks(vals):
-        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        t = torch.tensor(vals, dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.tolist()
