@@ -383,8 +383,8 @@ def main():
                        "k_planes_ms_per_step": plane_ms,
                        "stages_ms_diagnostic": stages_ms,
                        "chunks": nch, "cuda_graph": not args.no_graph,
-                       "overlap": "binning of chunk j+1 runs on a second stream under the "
-                                  "plane writes of chunk j",
+                       "overlap": ("binning of frame group j+1 on a second stream under the "
+                                   "plane kernel of group j" if nch > 1 else "none (one launch per stage)"),
                        "fused_grid": bool(p.fused)},
             "roofline": {"bound": "hbm", "kernel": "k_planes", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,

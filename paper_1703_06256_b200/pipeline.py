@@ -5,12 +5,12 @@ runs LUT binning -> integral planes -> cell grid (fused into the plane
 kernel when the scan lattice is regular) -> optional per-cell normalisation
 and window scores on the GPU, with no host synchronisation.
 
-The batch is processed in ``chunks`` frame groups on two streams: binning
-(instruction-bound, ~2 B/px of traffic) of chunk j+1 runs while the plane
-kernel (HBM-write-bound, 4*N_b B/px) of chunk j streams its planes out, so
-the binning time hides under the plane writes.  Frames are independent, so
-multi-GPU runs give each rank its own pipeline over its own frame shard (no
-collective).
+By default the whole batch is one launch per stage.  ``chunks > 1`` splits
+it into frame groups on two streams so that binning of group j+1 runs under
+the plane kernel of group j.  On B200 that measured slower: both kernels are
+issue/latency-bound, and the plane kernel loses more than the overlap saves
+(profiles/r1_c2_ncu_summary.md).  Frames are independent, so multi-GPU runs
+give each rank its own pipeline over its own frame shard, with no collective.
 """
 from __future__ import annotations
 
