@@ -49,7 +49,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-chunk", type=int, default=64, help="frames per H2D/compute/D2H chunk")
-    ap.add_argument("--e2e-slots", type=int, default=3, help="pipelines/streams in flight (e2e)")
+    ap.add_argument("--e2e-slots", type=int, default=4, help="pipelines/streams in flight (e2e)")
+    ap.add_argument("--e2e-tail", type=int, default=4,
+                    help="e2e: split the last chunk in this many pieces (shorter drain)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the timed steps (and the e2e step) eagerly, no CUDA graph")
     ap.add_argument("--pyr-chunk", type=int, default=16,
@@ -362,7 +364,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier,
-                      args.e2e_chunk, args.e2e_slots, not args.no_graph)
+                      args.e2e_chunk, args.e2e_slots, not args.no_graph, args.e2e_tail)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -489,39 +491,53 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
 
 
 def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, chunk=64, nslots=2,
-            use_graph=True):
+            use_graph=True, tail=1):
     """Per step: H2D of every frame from pinned host memory, the pipeline, and
-    D2H of the step's result, chunked over two streams so copies overlap
-    compute."""
+    D2H of the step's result, in frame chunks over `nslots` streams so the
+    copies in both directions overlap the kernels."""
     import torch
 
     from paper_1703_06256_b200 import synth
 
     chunk = max(1, min(nf, chunk))
-    nchunks = (nf + chunk - 1) // chunk
+    # job schedule: full chunks, with the last chunk split in `tail` pieces so
+    # the work left after the final H2D (its compute + D2H) is short
+    sizes = [chunk] * (nf // chunk) + ([nf % chunk] if nf % chunk else [])
+    if tail > 1 and sizes and sizes[-1] >= tail:
+        last = sizes.pop()
+        sizes += [last // tail] * (tail - 1) + [last - (last // tail) * (tail - 1)]
     weights, bias = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
-    slots = []
-    for _ in range(max(1, min(nslots, nchunks))):
-        q = H.HogPipeline(chunk, cfg.channels, cfg.height, cfg.width, cfg.bins,
-                          stride=cfg.stride, normalization=cfg.normalization, weights=weights,
-                          bias=bias, device=dev)
-        slots.append((q, torch.cuda.Stream(device=dev)))
+    nstreams = max(1, min(nslots, len(sizes)))
+    streams = [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
+    pipes = {}  # (stream, size) -> pipeline; jobs on one stream are serialised
+
+    def pipe(si, sz):
+        if (si, sz) not in pipes:
+            pipes[(si, sz)] = H.HogPipeline(sz, cfg.channels, cfg.height, cfg.width, cfg.bins,
+                                            stride=cfg.stride, normalization=cfg.normalization,
+                                            weights=weights, bias=bias, device=dev)
+        return pipes[(si, sz)]
+
+    jobs, a = [], 0
+    for j, sz in enumerate(sizes):
+        jobs.append((j % nstreams, a, a + sz, pipe(j % nstreams, sz)))
+        a += sz
     host_in = torch.from_numpy(frames).pin_memory()
-    res = slots[0][0].result()
+    res = jobs[0][3].result()
     host_out = torch.empty((nf,) + tuple(res.shape[1:]), dtype=res.dtype).pin_memory()
+
     def step():
         cur = torch.cuda.current_stream()
-        for s in (st for _, st in slots):
-            s.wait_stream(cur)
-        for j in range(nchunks):
-            q, st = slots[j % len(slots)]
-            a, b = j * chunk, min(nf, (j + 1) * chunk)
+        for st in streams:
+            st.wait_stream(cur)
+        for si, a, b, q in jobs:
+            st = streams[si]
             with torch.cuda.stream(st):
                 dst = q.frames.data if q.frames.pitch == cfg.width else q.frames.data[..., : cfg.width]
-                dst[: b - a].copy_(host_in[a:b], non_blocking=True)
+                dst.copy_(host_in[a:b], non_blocking=True)
                 q.run(stream=st)
-                host_out[a:b].copy_(q.result()[: b - a], non_blocking=True)
-        for _, st in slots:
+                host_out[a:b].copy_(q.result(), non_blocking=True)
+        for st in streams:
             cur.wait_stream(st)
 
     for _ in range(W):
@@ -553,7 +569,7 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
             "ms_per_step": ms, "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
             "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
             "result": "cell grid" if not cfg.scored else "window scores",
-            "chunk_frames": chunk, "streams": len(slots), "cuda_graph": bool(use_graph),
+            "chunk_frames": sizes, "streams": nstreams, "cuda_graph": bool(use_graph),
             "matches_device_run": ok}
 
 
