@@ -82,8 +82,10 @@ def naive_histogram(binmap: BinMap, r: Rect) -> np.ndarray:
     helper of the API; not on the accelerated path)."""
     check_rect(r, binmap.width, binmap.height)
     sub = np.asarray(binmap.cells[r.y0:r.y1, r.x0:r.x1]).ravel()
-    sub = sub[(sub >= 0) & (sub < binmap.bins)]
-    return np.bincount(sub, minlength=binmap.bins)[: binmap.bins].astype(np.int64)
+    sub = sub[sub >= 0]
+    if sub.size and int(sub.max()) >= binmap.bins:  # the reference's counts[v] += 1 raises here
+        raise IndexError("list index out of range")
+    return np.bincount(sub, minlength=binmap.bins).astype(np.int64)
 
 
 def normalize(values: np.ndarray, scheme: str) -> np.ndarray:

@@ -110,3 +110,8 @@ def test_rect_and_naive_histogram_host_helpers():
     with pytest.raises(H.RectOutOfBounds):
         H.naive_histogram(bm, H.Rect(0, 0, 11, 5))
     assert math.isclose(H.Rect(1, 2, 4, 6).area, 12)
+    # out-of-range bin values: the reference's list indexing raises IndexError
+    bad = cells.copy()
+    bad[3, 3] = 9
+    with pytest.raises(IndexError):
+        H.naive_histogram(H.BinMap(8, bad), H.Rect(0, 0, 10, 10))
