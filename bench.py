@@ -170,7 +170,23 @@ def cpu_run(cfg, frames, threads):
     mode = 1 if cfg.scored else (2 if cfg.normalization == "l2" else 0)
     w, b = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
     t0 = time.perf_counter()
-    O.run_batch(frames, lut, cfg.bins, 8, 64, 128, cfg.stride, mode, w, b, threads=threads)
+    if not cfg.pyramid_step:
+        O.run_batch(frames, lut, cfg.bins, 8, 64, 128, cfg.stride, mode, w, b, threads=threads)
+        return time.perf_counter() - t0
+    # pyramid (detector.py:224-269): every level resized from the original frame
+    # (resizes on a host thread pool; ctypes drops the GIL), then each level of
+    # all frames as one batch on `threads` threads
+    from concurrent.futures import ThreadPoolExecutor
+
+    n, C, H, W = frames.shape
+    g = O.Geometry(64, 128, 8, 1, 1, cfg.bins)
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        for (level, factor, lw, lh) in O.pyramid_levels(W, H, g, cfg.pyramid_step):
+            if level == 0:
+                batch = frames
+            else:
+                batch = np.stack(list(pool.map(lambda f: O.resize_bilinear(f, lw, lh), frames)))
+            O.run_batch(batch, lut, cfg.bins, 8, 64, 128, cfg.stride, mode, w, b, threads=threads)
     return time.perf_counter() - t0
 
 
@@ -179,11 +195,16 @@ def cpu_sample_size(cfg, frames1, threads, seconds):
     return max(threads, min(cfg.frames, int(seconds * threads / max(t1, 1e-3)))), t1
 
 
-def cpu_baseline(cfg, seconds):
+def cpu_baseline(cfg, seconds, frames=None):
+    """The oracle port on the host cores over a bounded sample of the workload
+    (`frames`, if given, are the benchmark's own frames: no regeneration)."""
     threads = host_threads()
-    probe = gen_frames(cfg, 0, 1)
+    probe = frames[:1] if frames is not None else gen_frames(cfg, 0, 1)
     count, t1 = cpu_sample_size(cfg, probe, threads, seconds)
-    frames = gen_frames(cfg, 0, count)
+    if frames is not None and len(frames) >= count:
+        frames = frames[:count]
+    else:
+        frames = gen_frames(cfg, 0, count)
     dt = cpu_run(cfg, frames, threads)
     px = count * cfg.height * cfg.width
     return {"value": px / dt / 1e6, "unit": "Mpixel/s", "cores": threads, "kind": "port",
@@ -368,7 +389,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, args.cpu_seconds)
+        cpu = cpu_baseline(cfg, args.cpu_seconds, frames)
 
     if rank == 0:
         line = {
@@ -461,6 +482,9 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
     ms = total_ms / K
     src_px = world * nf * cfg.height * cfg.width
     lvl_px = world * nf * p.pixels_per_frame()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.cpu_seconds, frames)
     peak, peak_src = measured_peak()
     achieved = plane_bytes / (plane_ms / 1e3) / 1e9
     step_bytes = p.bytes_alg_per_frame() * nf
@@ -483,7 +507,7 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
             "pipeline_roofline": {"achieved": step_bytes / (ms / 1e3) / 1e9, "peak": peak,
                                   "unit": "GB/s", "frac": step_bytes / (ms / 1e3) / 1e9 / peak,
                                   "alg_bytes_per_step": step_bytes},
-            "cpu_baseline": None, "e2e": None,
+            "cpu_baseline": cpu, "e2e": None,
             "gpu_launches": p.launches_per_run() * K, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
