@@ -353,3 +353,23 @@ def test_scores_rows_kernel(monkeypatch, bins, stride, h, w):
     for i in range(2):
         ref = O.scan_scores(O.integral_stack(O.gradient_map(frames[i], lut), bins), g, stride, wts, -0.125)
         np.testing.assert_allclose(got[0][i], ref, rtol=1e-9, atol=score_tol(wts))
+
+
+@pytest.mark.parametrize("chunks", [2, 3])
+def test_chunked_two_stream_pipeline_matches(chunks):
+    # frame groups on two streams (binning of group j+1 under the planes of
+    # group j) give the same bin maps, planes, grid and scores as one launch
+    cfg = synth.CONFIGS["c4"]
+    frames = np.ascontiguousarray(synth.make_batch(cfg, 7, 5)[:, :, :200, :320])
+    w, b = synth.make_weights(cfg)
+    outs = []
+    for ch in (1, chunks):
+        p = H.HogPipeline(5, 3, 200, 320, cfg.bins, stride=cfg.stride, weights=w, bias=b, chunks=ch)
+        assert p.chunks == ch
+        p.upload(frames)
+        p.run()
+        torch.cuda.synchronize()
+        outs.append((p.binmap_view().clone(), p.planes_view().clone(), p.grid.clone(),
+                     p.scores.clone()))
+    for a, c in zip(*outs):
+        assert torch.equal(a, c)
