@@ -1,0 +1,5 @@
+"""`fasthog.image_io` -> the B200 package (drop-in shim; see compat/fasthog/__init__.py)."""
+from paper_1703_06256_b200.image_io import *  # noqa: F401,F403
+from paper_1703_06256_b200 import image_io as _impl
+
+globals().update({k: getattr(_impl, k) for k in dir(_impl) if not k.startswith("__")})
