@@ -9,7 +9,7 @@ work (central differences, channel-max rule, LUT gather) runs in the
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
