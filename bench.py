@@ -54,6 +54,8 @@ def parse_args():
                     help="e2e: split the last chunk in this many pieces (shorter drain)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the timed steps (and the e2e step) eagerly, no CUDA graph")
+    ap.add_argument("--pyr-streams", type=int, default=0,
+                    help="c5: streams the pyramid levels are spread over (0: library default)")
     ap.add_argument("--pyr-chunk", type=int, default=16,
                     help="c5: frames per pyramid chunk (level buffers: ~7.8 GB of planes per frame)")
     return ap.parse_args()
@@ -77,10 +79,10 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(config_key):
+def ncu_traffic(config_key, key="k_planes_bytes_per_launch"):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        return json.load(open(p)).get(config_key, {}).get("k_planes_bytes_per_launch")
+        return json.load(open(p)).get(config_key, {}).get(key)
     except Exception:
         return None
 
@@ -444,7 +446,8 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
 
     p = H.PyramidPipeline(nf, cfg.channels, cfg.height, cfg.width, cfg.bins, stride=cfg.stride,
                           scale_step=cfg.pyramid_step, weights=weights, bias=bias,
-                          chunk=min(args.pyr_chunk, nf), device=dev)
+                          chunk=min(args.pyr_chunk, nf), device=dev,
+                          streams=args.pyr_streams or None)
     p.upload(frames)
     p.run()
     torch.cuda.synchronize()
@@ -480,8 +483,30 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
     plane_bytes = sum(b for _, _, b in pev)
     total_ms, plane_ms = max_over_ranks([total_ms, plane_ms])
     ms = total_ms / K
+    # diagnostic (outside the timed region): one pass with the levels on one
+    # stream, so the plane kernels' event durations are not shared with the
+    # concurrent levels' kernels
+    serial = None
+    if p.streams > 1:
+        saved, p.streams = p.streams, 1
+        sev = []
+        torch.cuda.synchronize()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record()
+        p.run(plane_events=sev)
+        s1.record()
+        torch.cuda.synchronize()
+        p.streams = saved
+        sp_ms = sum(e0.elapsed_time(e1) for e0, e1, _ in sev)
+        sp_gbs = sum(b for _, _, b in sev) / (sp_ms / 1e3) / 1e9
+        serial = {"step_ms": s0.elapsed_time(s1), "k_planes_ms": sp_ms, "k_planes_gbs": sp_gbs,
+                  "k_planes_frac": sp_gbs / measured_peak()[0]}
     src_px = world * nf * cfg.height * cfg.width
     lvl_px = world * nf * p.pixels_per_frame()
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, args.cpu_seconds, frames)
@@ -497,21 +522,88 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
             "dtype": "int32+f64", "data": "synthetic",
             "config": {"workload": workload_name(cfg), "frames_per_gpu": nf,
                        "levels": len(p.levels), "level_mpixel_per_s": lvl_px / (ms / 1e3) / 1e6,
-                       "frames_per_chunk": p.chunk,
+                       "frames_per_chunk": p.chunk, "level_streams": p.streams,
+                       "one_stream_diagnostic": serial,
                        "parallelism": f"frame-sharded x{world}, no collective",
                        "l2": f"inputs larger than L2 ({step_bytes / 1e9:.1f} GB per GPU per step)"},
             "roofline": {"bound": "hbm", "kernel": "k_planes", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "traffic_level0": {
+                             "bytes": ncu_traffic(cfg.key, "level0_k_planes_bytes_per_launch"),
+                             "alg_bytes": ncu_traffic(cfg.key, "level0_alg_bytes_per_launch"),
+                             "launch": "pyramid level 0 of a 16-frame chunk (ncu)"},
+                         "note": "plane-kernel event durations inside the timed region, where "
+                                 "levels on other streams run beside them (one-stream rate: "
+                                 "config.one_stream_diagnostic)",
                          "peak_source": peak_src, "launches_per_step": len(pev) // K,
                          "alg_bytes_per_step": plane_bytes / K},
             "pipeline_roofline": {"achieved": step_bytes / (ms / 1e3) / 1e9, "peak": peak,
                                   "unit": "GB/s", "frac": step_bytes / (ms / 1e3) / 1e9 / peak,
                                   "alg_bytes_per_step": step_bytes},
-            "cpu_baseline": cpu, "e2e": None,
+            "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": p.launches_per_run() * K, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     return 0
+
+
+def run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier):
+    """c5 end to end through PyramidPipeline: per step, H2D of every source
+    frame from pinned host memory (one copy per frame chunk on a copy stream;
+    chunk j's levels start when its frames have landed) and D2H of every
+    level's score maps (each level's slice leaves on a second copy stream as
+    soon as it is scored)."""
+    import torch
+
+    host_in = torch.from_numpy(frames).pin_memory()
+    host_out = [torch.empty(tuple(s.shape), dtype=s.dtype).pin_memory() for s in p.scores]
+    cin, cout = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    src = p.src.data
+
+    def step():
+        cur = torch.cuda.current_stream()
+        cin.wait_stream(cur)
+        cout.wait_stream(cur)
+        ready = {}
+        with torch.cuda.stream(cin):
+            for a in range(0, nf, p.chunk):
+                m = min(p.chunk, nf - a)
+                src[a:a + m].copy_(host_in[a:a + m], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cin)
+                ready[a] = ev
+
+        def chunk_ready(a, m, st):
+            st.wait_event(ready[a])
+
+        def level_done(level, a, m, st):
+            ev = torch.cuda.Event()
+            ev.record(st)
+            cout.wait_event(ev)
+            with torch.cuda.stream(cout):
+                host_out[level][a:a + m].copy_(p.scores[level][a:a + m], non_blocking=True)
+
+        p.run(cur, chunk_ready=chunk_ready, level_done=level_done)
+        cur.wait_stream(cout)
+
+    for _ in range(max(1, W)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(K):
+        step()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks([t0.elapsed_time(t1) / K])[0]
+    ok = all(torch.equal(h, s.cpu()) for h, s in zip(host_out, p.scores))
+    return {"value": world * nf * cfg.height * cfg.width / (ms / 1e3) / 1e6,
+            "unit": "Mpixel/s (source pixels)", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
+            "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in host_out)),
+            "result": "window scores of every pyramid level", "chunk_frames": p.chunk,
+            "streams": 3, "cuda_graph": False, "matches_device_run": ok}
 
 
 def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, chunk=64, nslots=2,

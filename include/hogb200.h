@@ -166,6 +166,14 @@ int hog_scores_lattice(const int32_t *grid, const double *den, int n, int ncy, i
                        int noy, int nox, int cells_x, int cells_y, int k, const double *weights,
                        double bias, double *scores, hog_stream_t stream);
 
+/* hog_scores_lattice over a uint8 cell grid (the plane kernel's byte grid,
+ * STAGE_GRID_U8; exact since cell counts <= cell^2 <= 255), unnormalised.
+ * Same windows, weights layout and fp64 accumulation; the byte grid quarters
+ * the kernel's staging footprint.  detector.py:140-154, descriptor.py:107-118. */
+int hog_scores_lattice_u8(const uint8_t *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
+                          int cells_x, int cells_y, int k, const double *weights, double bias,
+                          double *scores, hog_stream_t stream);
+
 /* detector.py:202-221 (_resize_bilinear): separable bilinear, pixel centres
  * aligned, float64 in the reference's operation order (no FMA contraction),
  * rint half-even, clip to 0..255.  ry = h / nh and rx = w / nw as computed by

@@ -35,6 +35,7 @@ SIGNATURES = {
     "hog_window_features": (_I, [_P, _I, _I, _I, _I, _P, _I, _P, _I, _I, _I, _I, _I, _I, _D,
                                  _P, _D, _P, _P, _P]),
     "hog_scores_lattice": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _D, _P, _P]),
+    "hog_scores_lattice_u8": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _D, _P, _P]),
     "hog_resize_bilinear": (_I, [_P, _I, _I, _I, _I, _L, _L, _L, _I, _I, _D, _D,
                                  _P, _L, _L, _L, _P]),
     "hog_integral16": (_I, [_P, _I, _I, _I, _L, _L, _I, _P, _L, _L, _L, _P]),

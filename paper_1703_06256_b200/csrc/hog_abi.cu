@@ -454,6 +454,22 @@ int hog_scores_lattice(const int32_t *grid, const double *den, int n, int ncy, i
     return check_launch("hog_scores_lattice");
 }
 
+int hog_scores_lattice_u8(const uint8_t *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
+                          int cells_x, int cells_y, int k, const double *wts, double bias,
+                          double *scores, hog_stream_t stream) {
+    g_err.clear();
+    if (n < 1 || noy < 1 || nox < 1 || bins < 1 || !grid || !wts || !scores)
+        return fail(HOG_EINVAL, "bad arguments");
+    if (k != 1 && k != 2) return fail(HOG_EINVAL, "lattice step ratio must be 1 or 2, got %d", k);
+    if (cells_x != 8)
+        return fail(HOG_EINVAL, "hog_scores_lattice_u8 is built for 8 cells across, got %d", cells_x);
+    if ((int64_t)(noy - 1) + (int64_t)(cells_y - 1) * k >= ncy || (int64_t)(nox - 1) + 7 * k >= ncx)
+        return fail(HOG_EINVAL, "window grid exceeds the cell lattice");
+    launch_scores_rows_u8(grid, n, ncy, ncx, bins, noy, nox, cells_y, k, wts, bias, scores,
+                          (cudaStream_t)stream);
+    return check_launch("hog_scores_lattice_u8");
+}
+
 int hog_resize_bilinear(const uint8_t *src, int n, int c, int h, int w, int64_t sp, int64_t scs,
                         int64_t sfs, int nh, int nw, double ry, double rx, uint8_t *dst,
                         int64_t dp, int64_t dcs, int64_t dfs, hog_stream_t stream) {

@@ -16,9 +16,18 @@
 //   with one pad word per TX columns: lane L reads column TX*L + j at word
 //   L*(TX*bins+1) + ..., an odd lane stride, so the reads are conflict-free.
 //   Per (row, bin) a lane converts its TX + 7K grid values to double once and
-//   reuses them for all SR_TY window rows (inactive rows multiply a zero
-//   weight row, which keeps the 4*TX accumulator chains independent and the
-//   FMA stream branch-free); weights are warp-broadcast LDS.128.
+//   reuses them for the SR_TY window rows that read that grid row (sr_row:
+//   one unrolled body per active-row mask, so no FMA is spent on rows that
+//   do not read it); weights are warp-broadcast LDS.128.
+//
+// uint8 grid (U8, cell counts <= 64 stored as bytes by the plane kernel): a
+//   staged row is the contiguous byte run of the grid row, copied by 16-byte
+//   cp.async.cg from the 16-byte-aligned address at or below it (zero-fill
+//   past the end of the grid), read at a per-row byte offset.  A slot is ~4x
+//   smaller than the int32 one: at N_b = 18 the int32 ring (96 KB) allowed
+//   one CTA (4 warps) per SM, the byte ring allows four.
+#include <type_traits>
+
 #include "hog_common.cuh"
 
 namespace hogb200 {
@@ -30,32 +39,87 @@ __device__ __forceinline__ void cp_async4(uint32_t *sdst, const int32_t *gsrc, b
                  "r"(valid ? 4 : 0)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(sdst)), "l"(gsrc),
+                 "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __host__ __device__ constexpr int sr_span(int tx, int k) { return 32 * tx + 7 * k; }
-// words of one staged grid row: ceil(span/tx) chunks of tx columns x bins + 1 pad
-__host__ __device__ inline int sr_slot_words(int bins, int tx, int k) {
+// words of one staged grid row: int32, ceil(span/tx) chunks of tx columns x
+// bins + 1 pad; uint8, the row's span*bins bytes + up to 15 bytes of leading
+// misalignment, in whole 16-byte chunks
+__host__ __device__ inline int sr_slot_words(int bins, int tx, int k, bool u8 = false) {
+    if (u8) return (sr_span(tx, k) * bins + 15 + 15) / 16 * 4;
     return ((sr_span(tx, k) + tx - 1) / tx) * (tx * bins + 1);
+}
+
+// One staged grid row against the window rows of MASK (bit u: window row
+// iyw + u reads this grid row, with weight row (rr - u) / K, rr = r - iyw).
+// Only active rows are computed: with a runtime zero-weight row instead, a
+// warp's 4 window rows would do 19 rows of FMAs for 16 useful ones (K = 1) or
+// twice the useful work (K = 2, where alternate rows are inactive).
+template <int K, int TX, int BINS, bool U8, int MASK>
+__device__ __forceinline__ void sr_row(double (&acc)[SR_TY][TX], const double *__restrict__ wsm,
+                                       int bins, int rr, const uint32_t *row, const uint8_t *rowb,
+                                       int ctb) {
+    constexpr int CX = 8, NG = TX / K + CX - 1;
+    const double *wu[SR_TY];
+#pragma unroll
+    for (int u = 0; u < SR_TY; ++u) wu[u] = wsm + ((MASK >> u) & 1 ? (rr - u) / K : 0) * bins * CX;
+    for (int bn = 0; bn < bins; ++bn) {
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+            double gs[NG];
+#pragma unroll
+            for (int j = 0; j < NG; ++j) {
+                const int c = p + K * j;  // column c0 + c
+                if constexpr (U8)
+                    gs[j] = (double)(uint32_t)rowb[c * bins + bn];
+                else
+                    gs[j] = (double)(int)row[(c / TX) * (ctb + 1) + (c % TX) * bins + bn];
+            }
+#pragma unroll
+            for (int cx = 0; cx < CX; cx += 2) {
+                double2 w2[SR_TY];
+#pragma unroll
+                for (int u = 0; u < SR_TY; ++u)
+                    if ((MASK >> u) & 1) w2[u] = *reinterpret_cast<const double2 *>(wu[u] + bn * CX + cx);
+#pragma unroll
+                for (int u = 0; u < SR_TY; ++u)
+                    if ((MASK >> u) & 1) {
+#pragma unroll
+                        for (int t = 0; t < TX / K; ++t) {
+                            acc[u][K * t + p] = fma(w2[u].x, gs[t + cx], acc[u][K * t + p]);
+                            acc[u][K * t + p] = fma(w2[u].y, gs[t + cx + 1], acc[u][K * t + p]);
+                        }
+                    }
+            }
+        }
+    }
 }
 
 // TX window columns per lane (32*TX per warp); BINS > 0: bin count known at
 // compile time (shared-memory offsets become immediates), 0: runtime `bins`.
-template <int K, int TX, int BINS>
+template <int K, int TX, int BINS, bool U8>
 __global__ void __launch_bounds__(32 * SR_WARPS, 3)
-k_scores_rows(const int32_t *__restrict__ grid, int ncy, int ncx, int bins_rt, int noy, int nox,
-              int cells_y, const double *__restrict__ wts, double bias, double *__restrict__ scores,
-              uint32_t magic) {
+k_scores_rows(const void *__restrict__ grid_v, int n, int ncy, int ncx, int bins_rt, int noy,
+              int nox, int cells_y, const double *__restrict__ wts, double bias,
+              double *__restrict__ scores, uint32_t magic) {
+    using T = typename std::conditional<U8, uint8_t, int32_t>::type;
+    const T *__restrict__ grid = static_cast<const T *>(grid_v);
     constexpr int CX = 8;
     constexpr int SPAN = sr_span(TX, K);  // grid columns a warp reads
     constexpr int NG = TX / K + CX - 1;   // grid values per (row, bin, parity)
     constexpr int COLS = 32 * TX;
     const int bins = BINS > 0 ? BINS : bins_rt;
     extern __shared__ __align__(16) double ssm[];
-    double *wsm = ssm;  // [cells_y + 1][bins][8]; row cells_y is zero (inactive window rows)
-    const int slotw = sr_slot_words(bins, TX, K);
+    double *wsm = ssm;  // [cells_y][bins][8]
+    const int slotw = sr_slot_words(bins, TX, K, U8);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t *ring = reinterpret_cast<uint32_t *>(ssm + (size_t)(cells_y + 1) * bins * CX) + warp * 2 * slotw;
+    uint32_t *ring = reinterpret_cast<uint32_t *>(ssm + (size_t)cells_y * bins * CX) + warp * 2 * slotw;
     const int tiles_x = (nox + COLS - 1) / COLS;
     const int tiles_y = (noy + SR_TY * SR_WARPS - 1) / (SR_TY * SR_WARPS);
     int bid = blockIdx.x;
@@ -65,11 +129,12 @@ k_scores_rows(const int32_t *__restrict__ grid, int ncy, int ncx, int bins_rt, i
     const int f = bid / tiles_y;
     const int ix0 = tx * COLS;
     const int iyw = ty * SR_TY * SR_WARPS + warp * SR_TY;  // this warp's first window row
-    const int32_t *gf = grid + (int64_t)f * ncy * ncx * bins;
+    const T *gf = grid + (int64_t)f * ncy * ncx * bins;
+    const int64_t gtotal = (int64_t)n * ncy * ncx * bins;  // grid elements (bytes if U8)
 
-    for (int i = threadIdx.x; i < (cells_y + 1) * CX * bins; i += blockDim.x) {
+    for (int i = threadIdx.x; i < cells_y * CX * bins; i += blockDim.x) {
         const int n = i % bins, cx = (i / bins) % CX, cy = i / (bins * CX);
-        wsm[(cy * bins + n) * CX + cx] = cy < cells_y ? wts[i] : 0.0;
+        wsm[(cy * bins + n) * CX + cx] = wts[i];
     }
     __syncthreads();  // the only CTA-wide barrier: weights staged
     if (iyw >= noy) return;
@@ -77,12 +142,27 @@ k_scores_rows(const int32_t *__restrict__ grid, int ncy, int ncx, int bins_rt, i
     const int nel = min(SPAN, ncx - ix0) * bins;  // words of a row inside the frame
     const int ctb = TX * bins;  // words of a chunk of TX columns (+1 pad word)
     auto stage = [&](int r, uint32_t *dst) {  // async copy of grid row r (this warp's columns)
-        const int32_t *src = gf + ((int64_t)r * ncx + ix0) * bins;
-        const bool rok = r < ncy;
-        for (int e = lane; e < SPAN * bins; e += 32) {
-            const int q = (int)__umulhi((uint32_t)e, magic);  // e / (TX*bins)
-            const bool ok = rok && e < nel;
-            cp_async4(dst + e + q, ok ? src + e : gf, ok);
+        if constexpr (U8) {
+            // bytes [a0, a0 + 16*nch) of the whole grid, a0 the 16-byte boundary at or below
+            // the row start; values past the frame's right edge only feed window columns
+            // that are not stored
+            const int64_t b0 = (((int64_t)f * ncy + r) * ncx + ix0) * bins;
+            const int64_t a0 = b0 & ~(int64_t)15;
+            const int nch = (int)((b0 - a0) + SPAN * bins + 15) / 16;
+            for (int e = lane; e < nch; e += 32) {
+                const int64_t o = a0 + 16 * (int64_t)e;
+                const int64_t left = gtotal - o;
+                const int bytes = left >= 16 ? 16 : (left > 0 ? (int)left : 0);
+                cp_async16(dst + 4 * e, bytes ? grid + o : grid, bytes);
+            }
+        } else {
+            const int32_t *src = gf + ((int64_t)r * ncx + ix0) * bins;
+            const bool rok = r < ncy;
+            for (int e = lane; e < SPAN * bins; e += 32) {
+                const int q = (int)__umulhi((uint32_t)e, magic);  // e / (TX*bins)
+                const bool ok = rok && e < nel;
+                cp_async4(dst + e + q, ok ? src + e : (const int32_t *)gf, ok);
+            }
         }
         cp_async_commit();
     };
@@ -103,39 +183,48 @@ k_scores_rows(const int32_t *__restrict__ grid, int ncy, int ncx, int bins_rt, i
         cp_async_wait_all();
         __syncwarp();  // row r visible to the warp; the other slot is free
         if (r < r_last) stage(r + 1, ring + (slot ^ 1) * slotw);
-        const double *wu[SR_TY];  // weight rows of grid row r for each window row (zero row if none)
+        const uint32_t *row = ring + slot * slotw + lbase;
+        const uint8_t *rowb = nullptr;
+        if constexpr (U8) {
+            const int64_t b0 = (((int64_t)f * ncy + r) * ncx + ix0) * bins;
+            rowb = reinterpret_cast<const uint8_t *>(ring + slot * slotw) + (int)(b0 & 15) +
+                   c0 * bins;
+        }
+        // window rows reading grid row r: u with d = rr - u in [0, (cells_y-1)*K], d % K == 0
+        const int rr = r - iyw;
+        int mask = 0;
 #pragma unroll
         for (int u = 0; u < SR_TY; ++u) {
-            const int d = r - (iyw + u);
-            const int cy = (d >= 0 && d % K == 0 && d / K < cells_y) ? d / K : cells_y;
-            wu[u] = wsm + cy * bins * CX;
+            const int d = rr - u;
+            if (d >= 0 && d % K == 0 && d / K < cells_y) mask |= 1 << u;
         }
-        const uint32_t *row = ring + slot * slotw + lbase;
-        for (int n = 0; n < bins; ++n) {
-#pragma unroll
-            for (int p = 0; p < K; ++p) {
-                double gs[NG];
-#pragma unroll
-                for (int j = 0; j < NG; ++j) {
-                    const int c = p + K * j;  // column c0 + c
-                    gs[j] = (double)(int)row[(c / TX) * (ctb + 1) + (c % TX) * bins + n];
-                }
-#pragma unroll
-                for (int cx = 0; cx < CX; cx += 2) {
-                    double2 w2[SR_TY];
-#pragma unroll
-                    for (int u = 0; u < SR_TY; ++u)
-                        w2[u] = *reinterpret_cast<const double2 *>(wu[u] + n * CX + cx);
-#pragma unroll
-                    for (int u = 0; u < SR_TY; ++u)
-#pragma unroll
-                        for (int t = 0; t < TX / K; ++t) {
-                            acc[u][K * t + p] = fma(w2[u].x, gs[t + cx], acc[u][K * t + p]);
-                            acc[u][K * t + p] = fma(w2[u].y, gs[t + cx + 1], acc[u][K * t + p]);
-                        }
-                }
+#define SR_ROW(M) sr_row<K, TX, BINS, U8, M>(acc, wsm, bins, rr, row, rowb, ctb)
+        if constexpr (K == 1) {
+            switch (mask) {
+                case 15: SR_ROW(15); break;
+                case 1: SR_ROW(1); break;
+                case 3: SR_ROW(3); break;
+                case 7: SR_ROW(7); break;
+                case 14: SR_ROW(14); break;
+                case 12: SR_ROW(12); break;
+                case 8: SR_ROW(8); break;
+                case 2: SR_ROW(2); break;  // runs of length 1-2 in the middle: cells_y < 4
+                case 4: SR_ROW(4); break;
+                case 6: SR_ROW(6); break;
+                default: break;  // masks are contiguous runs of bits: all listed
+            }
+        } else {
+            switch (mask) {
+                case 5: SR_ROW(5); break;
+                case 10: SR_ROW(10); break;
+                case 1: SR_ROW(1); break;
+                case 2: SR_ROW(2); break;
+                case 4: SR_ROW(4); break;
+                case 8: SR_ROW(8); break;
+                default: break;  // masks are runs of one parity: all listed
             }
         }
+#undef SR_ROW
     }
 #pragma unroll
     for (int u = 0; u < SR_TY; ++u) {
@@ -148,38 +237,40 @@ k_scores_rows(const int32_t *__restrict__ grid, int ncy, int ncx, int bins_rt, i
     }
 }
 
-size_t scores_rows_smem(int bins, int cells_y, int tx, int k) {
-    return sizeof(double) * (size_t)(cells_y + 1) * bins * 8 +
-           sizeof(uint32_t) * (size_t)SR_WARPS * 2 * sr_slot_words(bins, tx, k);
+size_t scores_rows_smem(int bins, int cells_y, int tx, int k, bool u8) {
+    return sizeof(double) * (size_t)cells_y * bins * 8 +
+           sizeof(uint32_t) * (size_t)SR_WARPS * 2 * sr_slot_words(bins, tx, k, u8);
 }
 
-template <int K, int TX, int BINS>
-void launch_rows_t(const int32_t *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
+template <int K, int TX, int BINS, bool U8>
+void launch_rows_t(const void *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
                    int cells_y, const double *wts, double bias, double *scores, cudaStream_t st) {
-    const size_t smem = scores_rows_smem(bins, cells_y, TX, K);
+    const size_t smem = scores_rows_smem(bins, cells_y, TX, K, U8);
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(k_scores_rows<K, TX, BINS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaFuncSetAttribute(k_scores_rows<K, TX, BINS, U8>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = smem;
     }
     // e / (TX bins) by multiply-high: exact for e < 2^20 (e < span * bins here)
     const uint32_t magic = (uint32_t)((0x100000000ull + TX * bins - 1) / (TX * bins));
     const int64_t blocks = (int64_t)n * ((noy + SR_TY * SR_WARPS - 1) / (SR_TY * SR_WARPS)) *
                            ((nox + 32 * TX - 1) / (32 * TX));
-    k_scores_rows<K, TX, BINS><<<(unsigned)blocks, 32 * SR_WARPS, smem, st>>>(
-        grid, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, magic);
+    k_scores_rows<K, TX, BINS, U8><<<(unsigned)blocks, 32 * SR_WARPS, smem, st>>>(
+        grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, magic);
 }
 
-template <int K, int TX>
-void launch_rows_b(const int32_t *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
+template <int K, int TX, bool U8>
+void launch_rows_b(const void *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
                    int cells_y, const double *wts, double bias, double *scores, cudaStream_t st) {
+#define SRB_ARGS grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, st
     switch (bins) {
-        case 8: return launch_rows_t<K, TX, 8>(grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, st);
-        case 9: return launch_rows_t<K, TX, 9>(grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, st);
-        case 18: return launch_rows_t<K, TX, 18>(grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, st);
-        default: return launch_rows_t<K, TX, 0>(grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, st);
+        case 8: return launch_rows_t<K, TX, 8, U8>(SRB_ARGS);
+        case 9: return launch_rows_t<K, TX, 9, U8>(SRB_ARGS);
+        case 18: return launch_rows_t<K, TX, 18, U8>(SRB_ARGS);
+        default: return launch_rows_t<K, TX, 0, U8>(SRB_ARGS);
     }
+#undef SRB_ARGS
 }
 
 // Window columns per lane: the candidate (TX / K integral) that wastes the
@@ -198,26 +289,39 @@ int pick_tx(int nox, int k) {
     return best;
 }
 
-void launch_scores_rows(const int32_t *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
-                        int cells_y, int k, const double *wts, double bias, double *scores,
-                        cudaStream_t st) {
+template <bool U8>
+void scores_rows_t(const void *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
+                   int cells_y, int k, const double *wts, double bias, double *scores,
+                   cudaStream_t st) {
     const int tx = pick_tx(nox, k);
 #define SR_ARGS grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, st
     if (k == 1) {
         switch (tx) {
-            case 2: return launch_rows_b<1, 2>(SR_ARGS);
-            case 3: return launch_rows_b<1, 3>(SR_ARGS);
-            case 4: return launch_rows_b<1, 4>(SR_ARGS);
-            case 5: return launch_rows_b<1, 5>(SR_ARGS);
-            default: return launch_rows_b<1, 6>(SR_ARGS);
+            case 2: return launch_rows_b<1, 2, U8>(SR_ARGS);
+            case 3: return launch_rows_b<1, 3, U8>(SR_ARGS);
+            case 4: return launch_rows_b<1, 4, U8>(SR_ARGS);
+            case 5: return launch_rows_b<1, 5, U8>(SR_ARGS);
+            default: return launch_rows_b<1, 6, U8>(SR_ARGS);
         }
     }
     switch (tx) {
-        case 2: return launch_rows_b<2, 2>(SR_ARGS);
-        case 4: return launch_rows_b<2, 4>(SR_ARGS);
-        default: return launch_rows_b<2, 6>(SR_ARGS);
+        case 2: return launch_rows_b<2, 2, U8>(SR_ARGS);
+        case 4: return launch_rows_b<2, 4, U8>(SR_ARGS);
+        default: return launch_rows_b<2, 6, U8>(SR_ARGS);
     }
 #undef SR_ARGS
+}
+
+void launch_scores_rows(const int32_t *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
+                        int cells_y, int k, const double *wts, double bias, double *scores,
+                        cudaStream_t st) {
+    scores_rows_t<false>(grid, n, ncy, ncx, bins, noy, nox, cells_y, k, wts, bias, scores, st);
+}
+
+void launch_scores_rows_u8(const uint8_t *grid, int n, int ncy, int ncx, int bins, int noy,
+                           int nox, int cells_y, int k, const double *wts, double bias,
+                           double *scores, cudaStream_t st) {
+    scores_rows_t<true>(grid, n, ncy, ncx, bins, noy, nox, cells_y, k, wts, bias, scores, st);
 }
 
 }  // namespace hogb200

@@ -65,13 +65,17 @@ class HogPipeline:
         self.frames = D.alloc_frames(n, channels, height, width, dev)
         self.binmap = D.alloc_binmap(n, height, width, dev)
         self.planes = D.alloc_planes(n, bins, height, width, dev)
-        # the fused grid is stored as uint8 when nothing downstream on the device
-        # reads it (cell counts <= cell^2 <= 255: exact, 4x fewer grid bytes)
-        u8_ok = self.fused and cell * cell <= 255 and weights is None and normalization == "none"
+        # the fused grid is stored as uint8 (cell counts <= cell^2 <= 255: exact,
+        # 4x fewer grid bytes) unless a device consumer needs int32: per-cell
+        # normalisation and the general window-feature path do; the lattice
+        # score kernel (8 cells across) reads bytes
+        u8_ok = (self.fused and cell * cell <= 255 and normalization == "none"
+                 and (weights is None or g.cells_x == 8))
         if grid_dtype not in ("auto", "int32", "uint8"):
             raise ValueError("grid_dtype must be 'auto', 'int32' or 'uint8'")
         if grid_dtype == "uint8" and not u8_ok:
-            raise ValueError("uint8 grid needs a fused lattice, cell*cell <= 255 and no device scores")
+            raise ValueError("uint8 grid needs a fused lattice, cell*cell <= 255, no normalisation "
+                             "and (if scored) 8 cells across")
         self.grid_u8 = grid_dtype == "uint8" or (grid_dtype == "auto" and u8_ok)
         self.grid = t.empty((n, self.ncy, self.ncx, bins),
                             dtype=t.uint8 if self.grid_u8 else t.int32, device=dev)
@@ -118,14 +122,15 @@ class HogPipeline:
             self.frames.data[..., : self.w].copy_(src, non_blocking=True)
 
     # -- the hot path -------------------------------------------------------
-    def _stage(self, j: int, stages: int, stream, events=None):
+    def _stage(self, j: int, stages: int, stream, events=None, frames_ptr=None):
         a, b = self.ranges[j]
         fr, bm, pl = self.frames, self.binmap, self.planes
         scr, sb = self.scratch[j]
         evs = None
         if events is not None:
             evs = (ctypes.c_void_p * 4)(*[e.cuda_event if e is not None else None for e in events])
-        _native.call("hog_pipeline", D.ptr(fr.data) + a * fr.fstride, b - a, self.c, self.h,
+        base = D.ptr(fr.data) if frames_ptr is None else frames_ptr
+        _native.call("hog_pipeline", base + a * fr.fstride, b - a, self.c, self.h,
                      self.w, fr.pitch, fr.cstride, fr.fstride, D.ptr(self.lut_dev), self.bins,
                      D.ptr(bm.data) + a * bm.fstride, bm.pitch, bm.fstride,
                      pl.ptr + 4 * a * pl.fstride, pl.pitch, pl.nstride, pl.fstride,
@@ -135,11 +140,14 @@ class HogPipeline:
                      D.ptr(scr), sb, stages | (_native.STAGE_GRID_U8 if self.grid_u8 else 0), evs,
                      D.stream_handle(stream))
 
-    def run(self, stream=None, plane_events=None):
+    def run(self, stream=None, plane_events=None, frames_ptr=None, scores_ptr=None):
         """Enqueue the whole batch; results are ready in `stream` order (default:
         current stream).  plane_events: optional per-chunk (start, end) pairs of
         recorded torch.cuda.Events bracketing each plane-kernel launch on the
-        stream it runs on."""
+        stream it runs on.  frames_ptr / scores_ptr: read the frames from / write
+        the scores to another device buffer of this pipeline's layout (the
+        pyramid's level 0 reads the source frames in place and every level
+        writes its slice of the pyramid's score maps directly)."""
         t = D.torch()
         main = stream if stream is not None else t.cuda.current_stream(self.device)
         if self.chunks == 1:
@@ -147,12 +155,12 @@ class HogPipeline:
             if plane_events is not None:
                 e0, e1 = plane_events[0]
                 evs = [None, None, e0, e1]
-            self._stage(0, _native.STAGE_ALL, main, evs)
+            self._stage(0, _native.STAGE_ALL, main, evs, frames_ptr)
         else:
             side = self.side
             side.wait_stream(main)
             for j in range(self.chunks):
-                self._stage(j, _native.STAGE_BIN | _native.STAGE_SCAN, main)
+                self._stage(j, _native.STAGE_BIN | _native.STAGE_SCAN, main, None, frames_ptr)
                 done = t.cuda.Event()
                 done.record(main)
                 side.wait_event(done)
@@ -160,9 +168,9 @@ class HogPipeline:
                 if plane_events is not None:
                     e0, e1 = plane_events[j]
                     evs = [None, None, e0, e1]
-                self._stage(j, _native.STAGE_PLANES, side, evs)
+                self._stage(j, _native.STAGE_PLANES, side, evs, frames_ptr)
             main.wait_stream(side)
-        self._post(main)
+        self._post(main, scores_ptr)
 
     def run_staged(self, events, stream=None):
         """Diagnostic: the whole batch as one chunk with 4 recorded events
@@ -182,9 +190,10 @@ class HogPipeline:
             self.ranges, self.scratch = saved
         self._post(main)
 
-    def _post(self, stream):
+    def _post(self, stream, scores_ptr=None):
         s = D.stream_handle(stream)
         pl = self.planes
+        sp = D.ptr(self.scores) if scores_ptr is None and self.scores is not None else scores_ptr
         if not self.fused:
             _native.call("hog_cell_grid", pl.ptr, self.n, self.h, self.w, self.bins, pl.pitch,
                          pl.nstride, pl.fstride, D.ptr(self.cx_dev), self.ncx,
@@ -194,18 +203,22 @@ class HogPipeline:
             _native.call("hog_cell_norm", D.ptr(self.grid), self.n, self.ncx * self.ncy,
                          self.bins, _NORM_CODE[g.normalization], eps_term(g.normalization),
                          D.ptr(self.denom), s)
-        if self.scores is not None and self.fused and g.cells_x == 8:
+        if self.scores is not None and self.fused and g.cells_x == 8 and self.grid_u8:
+            _native.call("hog_scores_lattice_u8", D.ptr(self.grid), self.n, self.ncy, self.ncx,
+                         self.bins, len(self.oys), len(self.oxs), g.cells_x, g.cells_y,
+                         self.cell // self.stride, D.ptr(self.w_dev), self.bias, sp, s)
+        elif self.scores is not None and self.fused and g.cells_x == 8:
             _native.call("hog_scores_lattice", D.ptr(self.grid),
                          D.ptr(self.denom) if self.denom is not None else None, self.n, self.ncy,
                          self.ncx, self.bins, len(self.oys), len(self.oxs), g.cells_x, g.cells_y,
                          self.cell // self.stride, D.ptr(self.w_dev), self.bias,
-                         D.ptr(self.scores), s)
+                         sp, s)
         elif self.scores is not None:
             _native.call("hog_window_features", D.ptr(self.grid), self.n, self.ncy, self.ncx,
                          self.bins, D.ptr(self.ri_dev), len(self.oys), D.ptr(self.ci_dev),
                          len(self.oxs), g.cells_x, g.cells_y, 1, 1, _NORM_CODE[g.normalization],
                          eps_term(g.normalization), D.ptr(self.w_dev), self.bias,
-                         D.ptr(self.scores), None, s)
+                         sp, None, s)
 
     def detections(self, threshold: float, iou_threshold: float | None = None, scale: float = 1.0):
         """Per-frame detection lists of the last run (needs weights): windows with
@@ -304,7 +317,8 @@ class PyramidPipeline:
 
     def __init__(self, n: int, channels: int, height: int, width: int, bins: int, *,
                  stride: int, scale_step: float, weights, bias: float = 0.0, cell: int = 8,
-                 window=(64, 128), chunk: int = 4, device=None, lut=None):
+                 window=(64, 128), chunk: int = 4, device=None, lut=None,
+                 streams: int | None = None):
         t = D.require_cuda()
         if scale_step <= 1.0:
             raise ValueError(f"scale_step must be > 1, got {scale_step}")
@@ -325,6 +339,13 @@ class PyramidPipeline:
                       for (_, _, w, h) in self.levels]
         self.scores = [t.empty((n,) + tuple(p.scores.shape[1:]), dtype=t.float64,
                                device=self.device) for p in self.pipes]
+        if streams is None:
+            import os
+
+            # measured on B200 (c5, 32 x 8K): 1 stream 85.1 ms, 2: 76.6, 3: 75.7
+            streams = int(os.environ.get("HOGB200_PYR_STREAMS", "3"))
+        self.streams = max(1, min(int(streams), len(self.levels)))
+        self._side = [t.cuda.Stream(device=self.device) for _ in range(self.streams - 1)]
 
     def upload(self, frames: np.ndarray):
         t = D.torch()
@@ -334,35 +355,67 @@ class PyramidPipeline:
         else:
             self.src.data[..., : self.w].copy_(src, non_blocking=True)
 
-    def run(self, stream=None, plane_events=None):
+    def run(self, stream=None, plane_events=None, chunk_ready=None, level_done=None):
         """plane_events: optional list; (start, end, algorithmic bytes) of every
-        plane-kernel launch is appended (events recorded on the launch stream)."""
+        plane-kernel launch is appended (events recorded on the launch stream).
+        chunk_ready(a, m, stream): called before `stream` first reads frames
+        [a, a+m) (e.g. to wait for their H2D copy); level_done(level, a, m,
+        stream): called once scores[level][a:a+m] are enqueued on `stream`
+        (e.g. to start their D2H).
+
+        Level 0 reads the source frames in place and every level writes its
+        score maps straight into ``scores[level]`` (no device copies).  Levels
+        are spread over ``self.streams`` streams (level i on stream i mod S),
+        so the launch-bound small levels and the FP64 score kernels run beside
+        the plane writes of other levels; one level's chunks stay in order on
+        its stream, which is what makes reusing its buffers safe."""
         t = D.torch()
         main = stream if stream is not None else t.cuda.current_stream(self.device)
-        s = D.stream_handle(main)
+        sts = [main] + self._side[: self.streams - 1]
+        for st in sts[1:]:
+            st.wait_stream(main)
         src = self.src
         for a in range(0, self.n, self.chunk):
             m = min(self.chunk, self.n - a)
-            for (level, factor, w, h), p in zip(self.levels, self.pipes):
+            if chunk_ready is not None:
+                for st in sts:
+                    chunk_ready(a, m, st)
+            # a partial last chunk runs through the level pipelines' own buffers
+            # (they process p.n frames: direct pointers would run past the batch)
+            whole = m == self.chunk
+            for i, ((level, factor, w, h), p) in enumerate(zip(self.levels, self.pipes)):
+                st = sts[i % len(sts)]
                 dst = p.frames
-                if level == 0:
-                    dst.data[:m].copy_(src.data[a:a + m])
-                else:
-                    _native.call("hog_resize_bilinear", D.ptr(src.data) + a * src.fstride, m,
-                                 self.c, self.h, self.w, src.pitch, src.cstride, src.fstride, h, w,
-                                 self.h / h, self.w / w, D.ptr(dst.data), dst.pitch, dst.cstride,
-                                 dst.fstride, s)
-                pev = None
-                if plane_events is not None:
-                    pev = []
-                    for _ in range(p.chunks):
-                        e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
-                        e0.record(main)
-                        e1.record(main)
-                        pev.append((e0, e1))
-                        plane_events.append((e0, e1, p.plane_kernel_bytes_per_frame() * p.n // p.chunks))
-                p.run(main, plane_events=pev)
-                self.scores[level][a:a + m].copy_(p.scores[:m])
+                with t.cuda.stream(st):
+                    if level == 0 and not whole:
+                        dst.data[:m].copy_(src.data[a:a + m])
+                    elif level != 0:
+                        _native.call("hog_resize_bilinear", D.ptr(src.data) + a * src.fstride, m,
+                                     self.c, self.h, self.w, src.pitch, src.cstride, src.fstride,
+                                     h, w, self.h / h, self.w / w, D.ptr(dst.data), dst.pitch,
+                                     dst.cstride, dst.fstride, D.stream_handle(st))
+                    pev = None
+                    if plane_events is not None:
+                        pev = []
+                        for _ in range(p.chunks):
+                            e0 = t.cuda.Event(enable_timing=True)
+                            e1 = t.cuda.Event(enable_timing=True)
+                            e0.record(st)
+                            e1.record(st)
+                            pev.append((e0, e1))
+                            plane_events.append(
+                                (e0, e1, p.plane_kernel_bytes_per_frame() * p.n // p.chunks))
+                    if whole:
+                        p.run(st, plane_events=pev,
+                              frames_ptr=D.ptr(src.data) + a * src.fstride if level == 0 else None,
+                              scores_ptr=D.ptr(self.scores[level][a]))
+                    else:
+                        p.run(st, plane_events=pev)
+                        self.scores[level][a:a + m].copy_(p.scores[:m])
+                if level_done is not None:
+                    level_done(level, a, m, st)
+        for st in sts[1:]:
+            main.wait_stream(st)
 
     def pixels_per_frame(self) -> int:
         """Pixels of every pyramid level of one frame."""

@@ -332,22 +332,26 @@ def test_tma_store_variant_matches(monkeypatch, shape):
 
 @pytest.mark.parametrize("bins,stride,h,w", [(18, 8, 300, 1000), (8, 4, 203, 611), (9, 8, 129, 64)])
 def test_scores_rows_kernel(monkeypatch, bins, stride, h, w):
-    # k_scores_rows (cp.async-staged grid rows, fp64 register tiles) against the
+    # k_scores_rows over the byte grid (default: 16-byte cp.async of misaligned
+    # grid rows -- every case here has rows that are not 16-byte multiples --
+    # zero-fill past the end of the grid) and over the int32 grid, against the
     # oracle's per-window dot products and against the first lattice kernel
     rng = np.random.default_rng(bins * 1000 + h)
     frames = synth.make_batch(synth.CONFIGS["c5"], 2, 1)[:, :, :h, :w].copy()
     frames = np.concatenate([frames, rng.integers(0, 256, frames.shape, dtype=np.uint8)])
     wts = rng.normal(0, 0.01, 128 * bins)
     got = []
-    for v1 in (None, "1"):
+    for gd, v1 in (("auto", None), ("int32", None), ("int32", "1")):
         if v1:
             monkeypatch.setenv("HOGB200_SCORES_V1", v1)
-        p = H.HogPipeline(2, 1, h, w, bins, stride=stride, weights=wts, bias=-0.125)
+        p = H.HogPipeline(2, 1, h, w, bins, stride=stride, weights=wts, bias=-0.125, grid_dtype=gd)
+        assert p.grid_u8 == (gd == "auto")
         p.upload(frames)
         p.run()
         torch.cuda.synchronize()
         got.append(p.scores.cpu().numpy())
     np.testing.assert_allclose(got[0], got[1], rtol=1e-12, atol=score_tol(wts))
+    np.testing.assert_allclose(got[0], got[2], rtol=1e-12, atol=score_tol(wts))
     g = O.Geometry(64, 128, 8, 1, 1, bins)
     lut = O.build_lut(bins)
     for i in range(2):
@@ -373,3 +377,24 @@ def test_chunked_two_stream_pipeline_matches(chunks):
                      p.scores.clone()))
     for a, c in zip(*outs):
         assert torch.equal(a, c)
+
+
+@pytest.mark.parametrize("wh,stride", [(16, 8), (24, 8), (16, 4), (40, 4)])
+def test_scores_rows_short_windows(wh, stride):
+    # windows 1-5 cells tall: the score kernel's active-row masks include the
+    # short runs (cells_y < 4) and, at stride 4, the one-parity runs
+    rng = np.random.default_rng(wh * 10 + stride)
+    frames = rng.integers(0, 256, (2, 1, 90, 260), dtype=np.uint8)
+    bins = 9
+    cells_y = wh // 8
+    wts = rng.normal(0, 0.01, 8 * cells_y * bins)
+    p = H.HogPipeline(2, 1, 90, 260, bins, stride=stride, window=(64, wh), weights=wts, bias=0.5)
+    assert p.fused and p.grid_u8
+    p.upload(frames)
+    p.run()
+    torch.cuda.synchronize()
+    g = O.Geometry(64, wh, 8, 1, 1, bins)
+    lut = O.build_lut(bins)
+    for i in range(2):
+        ref = O.scan_scores(O.integral_stack(O.gradient_map(frames[i], lut), bins), g, stride, wts, 0.5)
+        np.testing.assert_allclose(p.scores[i].cpu().numpy(), ref, rtol=1e-9, atol=score_tol(wts))

@@ -25,12 +25,16 @@ def score_tol(w):
     return 1e-12 * float(np.abs(w).sum()) * 64 + 1e-12
 
 
-def test_pyramid_pipeline_small_vs_oracle():
+@pytest.mark.parametrize("n,chunk,streams", [(2, 2, 1), (3, 2, 3)])
+def test_pyramid_pipeline_small_vs_oracle(n, chunk, streams):
+    """Whole chunks read the source frames in place and write the pyramid's
+    score maps directly; a partial last chunk goes through the level buffers;
+    levels spread over several streams give the same maps."""
     cfg = synth.CONFIGS["c5"]
-    frames = np.stack([synth.make_frame(cfg, i)[:, :300, :520] for i in range(2)])
+    frames = np.stack([synth.make_frame(cfg, i)[:, :300, :520] for i in range(n)])
     w, bias = synth.make_weights(cfg)
-    p = H.PyramidPipeline(2, 1, 300, 520, 18, stride=8, scale_step=1.2, weights=w, bias=bias,
-                          chunk=2)
+    p = H.PyramidPipeline(n, 1, 300, 520, 18, stride=8, scale_step=1.2, weights=w, bias=bias,
+                          chunk=chunk, streams=streams)
     p.upload(frames)
     p.run()
     torch.cuda.synchronize()
@@ -38,7 +42,7 @@ def test_pyramid_pipeline_small_vs_oracle():
     lut = O.build_lut(18)
     levels = O.pyramid_levels(520, 300, g, 1.2)
     assert [(lv, f, ww, hh) for lv, f, ww, hh in p.levels] == levels
-    for i in range(2):
+    for i in range(n):
         for (level, factor, lw, lh) in levels:
             img = frames[i] if level == 0 else O.resize_bilinear(frames[i], lw, lh)
             planes = O.integral_stack(O.gradient_map(img, lut), 18)
