@@ -609,8 +609,13 @@ def run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrie
 def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, chunk=64, nslots=2,
             use_graph=True, tail=1):
     """Per step: H2D of every frame from pinned host memory, the pipeline, and
-    D2H of the step's result, in frame chunks over `nslots` streams so the
-    copies in both directions overlap the kernels."""
+    D2H of the step's result, in frame chunks.  Each direction has ONE copy
+    stream, so chunks cross PCIe in order at full bandwidth (copies issued on
+    several streams share the link and all land late: measured with
+    tools/e2e_timeline.py); one compute stream runs each chunk as soon as it
+    has landed.  `nslots` buffer sets rotate, guarded by events (a chunk's H2D
+    waits until the chunk nslots back has been computed, its kernels until
+    that chunk's result has left)."""
     import torch
 
     from paper_1703_06256_b200 import synth
@@ -623,9 +628,9 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
         last = sizes.pop()
         sizes += [last // tail] * (tail - 1) + [last - (last // tail) * (tail - 1)]
     weights, bias = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
-    nstreams = max(1, min(nslots, len(sizes)))
-    streams = [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
-    pipes = {}  # (stream, size) -> pipeline; jobs on one stream are serialised
+    nslots = max(1, min(nslots, len(sizes)))
+    h2d, comp, d2h = (torch.cuda.Stream(device=dev) for _ in range(3))
+    pipes = {}  # (slot, size) -> pipeline
 
     def pipe(si, sz):
         if (si, sz) not in pipes:
@@ -636,24 +641,37 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
 
     jobs, a = [], 0
     for j, sz in enumerate(sizes):
-        jobs.append((j % nstreams, a, a + sz, pipe(j % nstreams, sz)))
+        jobs.append((a, a + sz, pipe(j % nslots, sz)))
         a += sz
     host_in = torch.from_numpy(frames).pin_memory()
-    res = jobs[0][3].result()
+    res = jobs[0][2].result()
     host_out = torch.empty((nf,) + tuple(res.shape[1:]), dtype=res.dtype).pin_memory()
 
     def step():
         cur = torch.cuda.current_stream()
-        for st in streams:
+        for st in (h2d, comp, d2h):
             st.wait_stream(cur)
-        for si, a, b, q in jobs:
-            st = streams[si]
-            with torch.cuda.stream(st):
+        landed, computed, left = [], [], []
+        for j, (a, b, q) in enumerate(jobs):
+            landed.append(torch.cuda.Event())
+            computed.append(torch.cuda.Event())
+            left.append(torch.cuda.Event())
+            if j >= nslots:
+                h2d.wait_event(computed[j - nslots])  # frames buffer free
+            with torch.cuda.stream(h2d):
                 dst = q.frames.data if q.frames.pitch == cfg.width else q.frames.data[..., : cfg.width]
                 dst.copy_(host_in[a:b], non_blocking=True)
-                q.run(stream=st)
+                landed[j].record(h2d)
+            comp.wait_event(landed[j])
+            if j >= nslots:
+                comp.wait_event(left[j - nslots])  # result buffer free
+            q.run(stream=comp)
+            computed[j].record(comp)
+            d2h.wait_event(computed[j])
+            with torch.cuda.stream(d2h):
                 host_out[a:b].copy_(q.result(), non_blocking=True)
-        for st in streams:
+                left[j].record(d2h)
+        for st in (h2d, comp, d2h):
             cur.wait_stream(st)
 
     for _ in range(W):
@@ -685,7 +703,8 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
             "ms_per_step": ms, "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
             "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
             "result": "cell grid" if not cfg.scored else "window scores",
-            "chunk_frames": sizes, "streams": nstreams, "cuda_graph": bool(use_graph),
+            "chunk_frames": sizes, "buffer_sets": nslots,
+            "streams": "1 H2D + 1 compute + 1 D2H (in-order copies)", "cuda_graph": bool(use_graph),
             "matches_device_run": ok}
 
 
