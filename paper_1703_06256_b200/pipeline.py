@@ -96,6 +96,7 @@ class HogPipeline:
                                                       cell if self.fused else 0))
             self.scratch.append((t.empty(max(sb, 256), dtype=t.uint8, device=dev), sb))
         self.side = t.cuda.Stream(device=dev) if self.chunks > 1 else None
+        self.post = t.cuda.Stream(device=dev) if self.chunks > 1 else None
         self.cx_dev = t.as_tensor(self.cell_xs.astype(np.int32), device=dev)
         self.cy_dev = t.as_tensor(self.cell_ys.astype(np.int32), device=dev)
         self.denom = None
@@ -157,8 +158,11 @@ class HogPipeline:
                 evs = [None, None, e0, e1]
             self._stage(0, _native.STAGE_ALL, main, evs, frames_ptr)
         else:
-            side = self.side
+            # three streams: binning of group j+1 (main), planes of group j (side)
+            # and the grid consumers (scores / normalisation) of group j-1 (post)
+            side, post = self.side, self.post
             side.wait_stream(main)
+            post.wait_stream(main)
             for j in range(self.chunks):
                 self._stage(j, _native.STAGE_BIN | _native.STAGE_SCAN, main, None, frames_ptr)
                 done = t.cuda.Event()
@@ -169,7 +173,13 @@ class HogPipeline:
                     e0, e1 = plane_events[j]
                     evs = [None, None, e0, e1]
                 self._stage(j, _native.STAGE_PLANES, side, evs, frames_ptr)
+                planed = t.cuda.Event()
+                planed.record(side)
+                post.wait_event(planed)
+                self._post(post, scores_ptr, *self.ranges[j])
             main.wait_stream(side)
+            main.wait_stream(post)
+            return
         self._post(main, scores_ptr)
 
     def run_staged(self, events, stream=None):
@@ -190,31 +200,39 @@ class HogPipeline:
             self.ranges, self.scratch = saved
         self._post(main)
 
-    def _post(self, stream, scores_ptr=None):
+    def _post(self, stream, scores_ptr=None, a: int = 0, b: int | None = None):
+        """Grid consumers (cell grid if not fused, per-cell denominators,
+        scores) for frames [a, b)."""
         s = D.stream_handle(stream)
         pl = self.planes
-        sp = D.ptr(self.scores) if scores_ptr is None and self.scores is not None else scores_ptr
+        b = self.n if b is None else b
+        n = b - a
+        cells = self.ncy * self.ncx
+        nwin = len(self.oys) * len(self.oxs)
+        gp = D.ptr(self.grid) + self.grid.element_size() * a * cells * self.bins
+        dp = D.ptr(self.denom) + 8 * a * cells if self.denom is not None else None
+        if self.scores is None:
+            sp = None
+        else:
+            sp = (D.ptr(self.scores) if scores_ptr is None else scores_ptr) + 8 * a * nwin
         if not self.fused:
-            _native.call("hog_cell_grid", pl.ptr, self.n, self.h, self.w, self.bins, pl.pitch,
-                         pl.nstride, pl.fstride, D.ptr(self.cx_dev), self.ncx,
-                         D.ptr(self.cy_dev), self.ncy, self.cell, D.ptr(self.grid), s)
+            _native.call("hog_cell_grid", pl.ptr + 4 * a * pl.fstride, n, self.h, self.w,
+                         self.bins, pl.pitch, pl.nstride, pl.fstride, D.ptr(self.cx_dev), self.ncx,
+                         D.ptr(self.cy_dev), self.ncy, self.cell, gp, s)
         g = self.geometry
         if self.denom is not None:
-            _native.call("hog_cell_norm", D.ptr(self.grid), self.n, self.ncx * self.ncy,
-                         self.bins, _NORM_CODE[g.normalization], eps_term(g.normalization),
-                         D.ptr(self.denom), s)
+            _native.call("hog_cell_norm", gp, n, cells, self.bins, _NORM_CODE[g.normalization],
+                         eps_term(g.normalization), dp, s)
         if self.scores is not None and self.fused and g.cells_x == 8 and self.grid_u8:
-            _native.call("hog_scores_lattice_u8", D.ptr(self.grid), self.n, self.ncy, self.ncx,
+            _native.call("hog_scores_lattice_u8", gp, n, self.ncy, self.ncx,
                          self.bins, len(self.oys), len(self.oxs), g.cells_x, g.cells_y,
                          self.cell // self.stride, D.ptr(self.w_dev), self.bias, sp, s)
         elif self.scores is not None and self.fused and g.cells_x == 8:
-            _native.call("hog_scores_lattice", D.ptr(self.grid),
-                         D.ptr(self.denom) if self.denom is not None else None, self.n, self.ncy,
+            _native.call("hog_scores_lattice", gp, dp, n, self.ncy,
                          self.ncx, self.bins, len(self.oys), len(self.oxs), g.cells_x, g.cells_y,
-                         self.cell // self.stride, D.ptr(self.w_dev), self.bias,
-                         sp, s)
+                         self.cell // self.stride, D.ptr(self.w_dev), self.bias, sp, s)
         elif self.scores is not None:
-            _native.call("hog_window_features", D.ptr(self.grid), self.n, self.ncy, self.ncx,
+            _native.call("hog_window_features", gp, n, self.ncy, self.ncx,
                          self.bins, D.ptr(self.ri_dev), len(self.oys), D.ptr(self.ci_dev),
                          len(self.oxs), g.cells_x, g.cells_y, 1, 1, _NORM_CODE[g.normalization],
                          eps_term(g.normalization), D.ptr(self.w_dev), self.bias,
@@ -247,10 +265,9 @@ class HogPipeline:
 
     def launches_per_run(self) -> int:
         k = 3 * self.chunks  # grad_bin + carry scan + planes per chunk
-        k += 0 if self.fused else 1
-        k += 1 if self.denom is not None else 0
-        k += 1 if self.scores is not None else 0
-        return k
+        post = (0 if self.fused else 1) + (1 if self.denom is not None else 0) + \
+            (1 if self.scores is not None else 0)
+        return k + post * self.chunks  # grid consumers run per chunk
 
     # -- views ----------------------------------------------------------------
     def planes_view(self):

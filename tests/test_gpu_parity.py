@@ -379,6 +379,32 @@ def test_chunked_two_stream_pipeline_matches(chunks):
         assert torch.equal(a, c)
 
 
+@pytest.mark.parametrize("stride,norm", [(8, "l2"), (12, "none"), (12, "l1")])
+def test_chunked_pipeline_grid_consumers(stride, norm):
+    # per-group grid consumers on the third stream: per-cell denominators +
+    # int32 lattice scores (fused, normalised), and the general cell-grid +
+    # window-feature path (stride 12: no regular lattice), equal to one launch
+    cfg = synth.CONFIGS["c3"]
+    frames = np.ascontiguousarray(synth.make_batch(cfg, 9, 5)[:, :, :260, :330])
+    w = np.random.default_rng(stride).normal(0, 0.01, 128 * cfg.bins)
+    outs = []
+    for ch in (1, 3):
+        p = H.HogPipeline(5, 1, 260, 330, cfg.bins, stride=stride, normalization=norm, weights=w,
+                          bias=0.1, chunks=ch)
+        assert p.fused == (stride == 8)
+        p.upload(frames)
+        p.run()
+        torch.cuda.synchronize()
+        outs.append([p.grid.clone(), p.scores.clone()] +
+                    ([p.denom.clone()] if p.denom is not None else []))
+    for a, c in zip(*outs):
+        assert torch.equal(a, c)
+    g = O.Geometry(64, 128, 8, 1, 1, cfg.bins, norm)
+    lut = O.build_lut(cfg.bins)
+    ref = O.scan_scores(O.integral_stack(O.gradient_map(frames[4], lut), cfg.bins), g, stride, w, 0.1)
+    np.testing.assert_allclose(outs[1][1][4].cpu().numpy(), ref, rtol=1e-9, atol=score_tol(w))
+
+
 @pytest.mark.parametrize("wh,stride", [(16, 8), (24, 8), (16, 4), (40, 4)])
 def test_scores_rows_short_windows(wh, stride):
     # windows 1-5 cells tall: the score kernel's active-row masks include the
