@@ -263,6 +263,18 @@ __device__ __forceinline__ void store_cols(const TileGeom &g, const Scratch &sc,
 }
 
 
+// The dynamic shared-memory opt-in (cudaFuncSetAttribute) is per device: a
+// launcher remembers, per device, the largest size it has set for its kernel.
+constexpr int HOG_MAX_DEVICES = 64;
+inline bool smem_optin_needed(size_t (&done)[HOG_MAX_DEVICES], size_t smem) {
+    if (smem <= 48 * 1024) return false;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= HOG_MAX_DEVICES) return true;
+    if (smem <= done[dev]) return false;
+    done[dev] = smem;
+    return true;
+}
+
 inline unsigned blocks_for_warps(int64_t warps) {
     return (unsigned)((warps + (K_THREADS / 32) - 1) / (K_THREADS / 32));
 }

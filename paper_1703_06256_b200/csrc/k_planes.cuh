@@ -705,12 +705,10 @@ void launch_planes_vc(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut 
                       const GridOut &go, const TileGeom &g, const Scratch &sc, const FusedIn &fi,
                       cudaStream_t st) {
     const size_t smem = (size_t)k2_smem_words(g, KR) * 4;
-    static size_t configured = 0;  // per instantiation
-    if (smem > 48 * 1024 && smem > configured) {
+    static size_t configured[HOG_MAX_DEVICES] = {};  // per instantiation and device
+    if (smem_optin_needed(configured, smem))
         cudaFuncSetAttribute(k_planes<NW, KR, VC, VEC, CH, TMA>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
     k_planes<NW, KR, VC, VEC, CH, TMA>
         <<<(unsigned)((int64_t)g.n * g.nb2), 32 * (g.NWARP + (TMA ? 1 : 0)), smem, st>>>(
             bm, bp, bfs, po, go, g, sc, fi);

@@ -246,12 +246,10 @@ template <int K, int TX, int BINS, bool U8>
 void launch_rows_t(const void *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
                    int cells_y, const double *wts, double bias, double *scores, cudaStream_t st) {
     const size_t smem = scores_rows_smem(bins, cells_y, TX, K, U8);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    static size_t configured[HOG_MAX_DEVICES] = {};
+    if (smem_optin_needed(configured, smem))
         cudaFuncSetAttribute(k_scores_rows<K, TX, BINS, U8>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
     // e / (TX bins) by multiply-high: exact for e < 2^20 (e < span * bins here)
     const uint32_t magic = (uint32_t)((0x100000000ull + TX * bins - 1) / (TX * bins));
     const int64_t blocks = (int64_t)n * ((noy + SR_TY * SR_WARPS - 1) / (SR_TY * SR_WARPS)) *

@@ -345,12 +345,10 @@ void launch_scores_lattice(const int32_t *grid, const double *den, int n, int nc
     const int span = SC_COLS + 7 * k;
     const size_t smem =
         sizeof(double) * ((size_t)cells_y * bins * 8 + 2 * (size_t)bins * (span + span / 8 + 1));
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    static size_t configured[HOG_MAX_DEVICES] = {};
+    if (smem_optin_needed(configured, smem))
         cudaFuncSetAttribute(k_scores_lattice<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        configured = smem;
-    }
     const int64_t blocks = (int64_t)n * ((noy + SC_TY * SC_YG - 1) / (SC_TY * SC_YG)) *
                            ((nox + SC_COLS - 1) / SC_COLS);
     k_scores_lattice<8><<<(unsigned)blocks, 32 * SC_YG, smem, st>>>(grid, den, ncy, ncx, bins, noy,
