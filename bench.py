@@ -410,7 +410,9 @@ def main():
                        "chunks": nch, "cuda_graph": not args.no_graph,
                        "overlap": ("binning of frame group j+1 on a second stream under the "
                                    "plane kernel of group j" if nch > 1 else "none (one launch per stage)"),
-                       "fused_grid": bool(p.fused)},
+                       "fused_grid": bool(p.fused),
+                       "band_rows": {"used": p.band_rows, "library_default": p.auto_band_rows(),
+                                     "tuned_ms": p.band_rows_timings}},
             "roofline": {"bound": "hbm", "kernel": "k_planes", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_src,
@@ -523,6 +525,7 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
             "config": {"workload": workload_name(cfg), "frames_per_gpu": nf,
                        "levels": len(p.levels), "level_mpixel_per_s": lvl_px / (ms / 1e3) / 1e6,
                        "frames_per_chunk": p.chunk, "level_streams": p.streams,
+                       "band_rows_per_level": [q.band_rows for q in p.pipes],
                        "one_stream_diagnostic": serial,
                        "parallelism": f"frame-sharded x{world}, no collective",
                        "l2": f"inputs larger than L2 ({step_bytes / 1e9:.1f} GB per GPU per step)"},

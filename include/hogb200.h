@@ -73,8 +73,17 @@ int hog_grad_bin(const uint8_t *img, int n, int c, int h, int w,
                  int8_t *binmap, int64_t bm_pitch, int64_t bm_fstride,
                  hog_stream_t stream);
 
-/* Scratch needed by hog_integral / hog_pipeline for this shape. */
+/* Scratch needed by hog_integral / hog_pipeline for this shape (at the band
+ * rows in effect on the calling thread, see hog_set_band_rows). */
 size_t hog_scratch_bytes(int n, int h, int w, int bins, int stride, int cell);
+
+/* Band rows R (plane rows per CTA of the integral-plane kernel) used by this
+ * thread's following hog_pipeline / hog_integral / hog_scratch_bytes calls;
+ * rows < 8 restores the automatic choice.  Any R gives the same planes; it
+ * only changes the tiling (the batched pipeline measures a few per shape and
+ * keeps the fastest).  hog_get_band_rows returns the R a call would use. */
+void hog_set_band_rows(int rows);
+int hog_get_band_rows(int n, int h, int w, int bins, int stride, int cell);
 
 /* integral.py:58-87 (build_integral_stack, 32-bit accumulators): the N_b
  * padded summed-area tables of a bin map, every plane element written once. */

@@ -24,6 +24,8 @@ SIGNATURES = {
     "hog_plane_pitch": (_L, [_I]),
     "hog_grad_bin": (_I, [_P, _I, _I, _I, _I, _L, _L, _L, _P, _I, _P, _L, _L, _P]),
     "hog_scratch_bytes": (_SZ, [_I, _I, _I, _I, _I, _I]),
+    "hog_set_band_rows": (None, [_I]),
+    "hog_get_band_rows": (_I, [_I, _I, _I, _I, _I, _I]),
     "hog_integral": (_I, [_P, _I, _I, _I, _L, _L, _I, _P, _L, _L, _L, _P, _SZ, _P]),
     "hog_pipeline": (_I, [_P, _I, _I, _I, _I, _L, _L, _L, _P, _I, _P, _L, _L,
                           _P, _L, _L, _L, _I, _I, _I, _I, _P, _P, _SZ, _I, _P, _P]),

@@ -50,6 +50,10 @@ static int env_int(const char *name, int dflt) {
     return (e && *e) ? atoi(e) : dflt;
 }
 
+// Band rows R of the plane kernel for this thread's next calls (0: automatic).
+// Thread-local: a caller sets it around its own launches.
+thread_local int g_band_rows = 0;
+
 // k_planes shared memory per CTA must allow two resident CTAs per SM
 constexpr int K2_SMEM_BUDGET = 113 * 1024;
 
@@ -95,7 +99,9 @@ TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int ce
     g.Wc = g.nc1 * CHUNK;
     int R = 128;
     const char *env = getenv("HOGB200_BAND_ROWS");
-    if (env && atoi(env) >= 8) {
+    if (g_band_rows >= 8) {  // hog_set_band_rows: the caller measured this shape
+        R = g_band_rows;
+    } else if (env && atoi(env) >= 8) {
         R = atoi(env);
     } else {
         while (R > 16 && (int64_t)n * (h / R + 1) * g.NWARP < 148 * 32) R /= 2;
@@ -375,6 +381,13 @@ int hog_pipeline(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
     return pipeline_impl(img, n, c, h, w, ip, ics, ifs, lut, bins, bm, bp, bfs, pl, pp, pns, pfs,
                          cell, stride, ncx, ncy, grid, scratch, sbytes, stages, stage_events, 0, 0,
                          nullptr, 0, stream);
+}
+
+void hog_set_band_rows(int rows) { g_band_rows = rows >= 8 ? rows : 0; }
+
+int hog_get_band_rows(int n, int h, int w, int bins, int stride, int cell) {
+    if (n < 1 || h < 1 || w < 1 || bins < 1) return 0;
+    return make_geom(n, h, w, bins, stride > 0 && cell > 0, stride, cell, true, false).R;
 }
 
 int hog_pipeline_slab(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int64_t ics,

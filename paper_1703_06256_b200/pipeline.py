@@ -34,6 +34,12 @@ def regular_lattice(cell_xs, cell_ys, stride: int, cell: int, bins: int) -> bool
     return True
 
 
+def _tune_enabled() -> bool:
+    import os
+
+    return os.environ.get("HOGB200_TUNE", "1") != "0"
+
+
 def default_chunks(n: int, pixels_per_frame: int) -> int:
     """Frame groups for the binning/plane overlap.  Measured on B200 (c2): the
     plane kernel loses more to a co-running binning kernel than the overlap
@@ -48,7 +54,7 @@ class HogPipeline:
     def __init__(self, n: int, channels: int, height: int, width: int, bins: int, *,
                  stride: int, cell: int = 8, window=(64, 128), normalization: str = "none",
                  weights=None, bias: float = 0.0, lut=None, device=None, chunks: int | None = None,
-                 grid_dtype: str = "auto"):
+                 grid_dtype: str = "auto", band_rows: int | None = None):
         t = D.require_cuda()
         self.n, self.c, self.h, self.w, self.bins = n, channels, height, width, bins
         self.stride, self.cell = stride, cell
@@ -89,12 +95,9 @@ class HogPipeline:
             b = a + base + (1 if j < rem else 0)
             self.ranges.append((a, b))
             a = b
+        self.band_rows = 0 if band_rows is None else int(band_rows)  # 0: library's choice
         self.scratch = []
-        for (a, b) in self.ranges:
-            sb = int(_native.load().hog_scratch_bytes(b - a, height, width, bins,
-                                                      stride if self.fused else 0,
-                                                      cell if self.fused else 0))
-            self.scratch.append((t.empty(max(sb, 256), dtype=t.uint8, device=dev), sb))
+        self._alloc_scratch()
         self.side = t.cuda.Stream(device=dev) if self.chunks > 1 else None
         self.post = t.cuda.Stream(device=dev) if self.chunks > 1 else None
         self.cx_dev = t.as_tensor(self.cell_xs.astype(np.int32), device=dev)
@@ -112,6 +115,73 @@ class HogPipeline:
             self.w_dev = t.as_tensor(self.weights, device=dev)
             self.ri_dev = t.as_tensor(self.row_idx.astype(np.int32), device=dev)
             self.ci_dev = t.as_tensor(self.col_idx.astype(np.int32), device=dev)
+        self.band_rows_timings = None
+        if band_rows is None and self.chunks == 1 and _tune_enabled():
+            self.band_rows = self._tune_band_rows()
+
+    # -- plane-kernel band rows ---------------------------------------------
+    def _scratch_bytes(self, a: int, b: int) -> int:
+        lib = _native.load()
+        lib.hog_set_band_rows(self.band_rows)
+        try:
+            return int(lib.hog_scratch_bytes(b - a, self.h, self.w, self.bins,
+                                             self.stride if self.fused else 0,
+                                             self.cell if self.fused else 0))
+        finally:
+            lib.hog_set_band_rows(0)
+
+    def _alloc_scratch(self):
+        t = D.torch()
+        out = []
+        for j, (a, b) in enumerate(self.ranges):
+            sb = self._scratch_bytes(a, b)
+            old = self.scratch[j][0] if j < len(self.scratch) else None
+            buf = old if old is not None and old.numel() >= sb else \
+                t.empty(max(sb, 256), dtype=t.uint8, device=self.device)
+            out.append((buf, sb))
+        self.scratch = out
+
+    def auto_band_rows(self) -> int:
+        """The library's own choice of band rows for this shape."""
+        return int(_native.load().hog_get_band_rows(self.n, self.h, self.w, self.bins,
+                                                    self.stride if self.fused else 0,
+                                                    self.cell if self.fused else 0))
+
+    def _tune_band_rows(self) -> int:
+        """Time binning + carry scan + planes (+ grid) at a few band rows on this
+        pipeline's own buffers and keep the fastest; the automatic choice stays
+        unless another is > 2 % faster.  Measured on B200, the best R moves
+        with the CTA-wave count of the shape (profiles/r1b_band_sweep.txt: c4
+        best at 80, 8K pyramid level 1 at 40, c2/c3/level 0 at the automatic R).
+        Any R gives bit-identical outputs; only the tiling changes."""
+        t = D.torch()
+        auto = self.auto_band_rows()
+        cands = [auto] + [r for r in (32, 40, 48, 64, 80, 96, 128)
+                          if r != auto and r <= max(D.round_up(self.h + 1, 8), 32)]
+        stream = t.cuda.current_stream(self.device)
+        times = {}
+        for r in cands:
+            self.band_rows = r
+            self._alloc_scratch()
+            best = None
+            for it in range(3):
+                e0 = t.cuda.Event(enable_timing=True)
+                e1 = t.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                self._stage(0, _native.STAGE_ALL, stream)
+                e1.record(stream)
+                e1.synchronize()
+                if it:
+                    ms = e0.elapsed_time(e1)
+                    best = ms if best is None else min(best, ms)
+            times[r] = best
+        pick = min(times, key=times.get)
+        if times[pick] > 0.98 * times[auto]:
+            pick = auto
+        self.band_rows_timings = times
+        self.band_rows = pick
+        self._alloc_scratch()
+        return pick
 
     # -- data movement ------------------------------------------------------
     def upload(self, frames: np.ndarray, stream=None):
@@ -131,6 +201,14 @@ class HogPipeline:
         if events is not None:
             evs = (ctypes.c_void_p * 4)(*[e.cuda_event if e is not None else None for e in events])
         base = D.ptr(fr.data) if frames_ptr is None else frames_ptr
+        lib = _native.load()
+        lib.hog_set_band_rows(self.band_rows)
+        try:
+            self._pipeline_call(base, a, b, fr, bm, pl, scr, sb, stages, evs, stream)
+        finally:
+            lib.hog_set_band_rows(0)
+
+    def _pipeline_call(self, base, a, b, fr, bm, pl, scr, sb, stages, evs, stream):
         _native.call("hog_pipeline", base + a * fr.fstride, b - a, self.c, self.h,
                      self.w, fr.pitch, fr.cstride, fr.fstride, D.ptr(self.lut_dev), self.bins,
                      D.ptr(bm.data) + a * bm.fstride, bm.pitch, bm.fstride,

@@ -424,3 +424,30 @@ def test_scores_rows_short_windows(wh, stride):
     for i in range(2):
         ref = O.scan_scores(O.integral_stack(O.gradient_map(frames[i], lut), bins), g, stride, wts, 0.5)
         np.testing.assert_allclose(p.scores[i].cpu().numpy(), ref, rtol=1e-9, atol=score_tol(wts))
+
+
+@pytest.mark.parametrize("key,crop", [("c4", (300, 1280)), ("c3", (400, 1000)), ("c5", (260, 2100)),
+                                      ("c2", None)])
+def test_band_rows_invariance(key, crop):
+    # the plane kernel's band rows only change the tiling: every R gives the
+    # same bin map, planes and grid (and the oracle's planes); c5's crop is
+    # 2100 wide with N_b = 18 (several super-strips per CTA), c4 is RGB
+    # with 8 columns per lane
+    cfg = synth.CONFIGS[key]
+    h, w = crop or (cfg.height, cfg.width)
+    frames = np.ascontiguousarray(synth.make_batch(cfg, 13, 2)[:, :, :h, :w])
+    outs = []
+    for rows in (16, 40, 96, 240, None):
+        p = H.HogPipeline(2, cfg.channels, h, w, cfg.bins, stride=cfg.stride, band_rows=rows)
+        if rows is None:
+            assert p.band_rows in p.band_rows_timings  # tuned among the measured candidates
+        p.upload(frames)
+        p.run()
+        torch.cuda.synchronize()
+        outs.append((p.binmap_view().clone(), p.planes_view().clone(), p.grid.clone()))
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert torch.equal(a, b)
+    lut = O.build_lut(cfg.bins)
+    ref = O.integral_stack(O.gradient_map(frames[1], lut), cfg.bins)
+    assert np.array_equal(outs[0][1][1].cpu().numpy().view(np.uint32), ref)
