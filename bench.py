@@ -54,6 +54,8 @@ def parse_args():
                     help="e2e: split the last chunk in this many pieces (shorter drain)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the timed steps (and the e2e step) eagerly, no CUDA graph")
+    ap.add_argument("--pipelined", type=int, default=1,
+                    help="scored configs: batch k's scores run beside batch k+1's binning")
     ap.add_argument("--pyr-streams", type=int, default=0,
                     help="c5: streams the pyramid levels are spread over (0: library default)")
     ap.add_argument("--pyr-chunk", type=int, default=16,
@@ -335,9 +337,13 @@ def main():
             e1.record()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
+    pipelined = bool(args.pipelined and p.scores is not None and p.chunks == 1)
+
     def timed_steps():
+        p.join()
         for i in range(K):
-            p.run(plane_events=pev[i])
+            p.run(plane_events=pev[i], pipelined=pipelined)
+        p.join()
 
     launch = timed_steps
     if not args.no_graph:
@@ -411,6 +417,7 @@ def main():
                        "overlap": ("binning of frame group j+1 on a second stream under the "
                                    "plane kernel of group j" if nch > 1 else "none (one launch per stage)"),
                        "fused_grid": bool(p.fused),
+                       "pipelined_batches": pipelined,
                        "band_rows": {"used": p.band_rows, "library_default": p.auto_band_rows(),
                                      "tuned_ms": p.band_rows_timings}},
             "roofline": {"bound": "hbm", "kernel": "k_planes", "achieved": achieved,

@@ -100,6 +100,7 @@ class HogPipeline:
         self._alloc_scratch()
         self.side = t.cuda.Stream(device=dev) if self.chunks > 1 else None
         self.post = t.cuda.Stream(device=dev) if self.chunks > 1 else None
+        self._post_done = None  # event: scores of the last pipelined run
         self.cx_dev = t.as_tensor(self.cell_xs.astype(np.int32), device=dev)
         self.cy_dev = t.as_tensor(self.cell_ys.astype(np.int32), device=dev)
         self.denom = None
@@ -219,7 +220,8 @@ class HogPipeline:
                      D.ptr(scr), sb, stages | (_native.STAGE_GRID_U8 if self.grid_u8 else 0), evs,
                      D.stream_handle(stream))
 
-    def run(self, stream=None, plane_events=None, frames_ptr=None, scores_ptr=None):
+    def run(self, stream=None, plane_events=None, frames_ptr=None, scores_ptr=None,
+            pipelined: bool = False):
         """Enqueue the whole batch; results are ready in `stream` order (default:
         current stream).  plane_events: optional per-chunk (start, end) pairs of
         recorded torch.cuda.Events bracketing each plane-kernel launch on the
@@ -229,6 +231,29 @@ class HogPipeline:
         writes its slice of the pyramid's score maps directly)."""
         t = D.torch()
         main = stream if stream is not None else t.cuda.current_stream(self.device)
+        if pipelined and self.chunks == 1 and self.scores is not None:
+            # consecutive batches overlap: this batch's binning + carry scan run
+            # while the previous batch's scores are still computing (on
+            # self.post); its plane kernel waits for them (it rewrites the grid
+            # they read).  Results are ready after join().
+            if self.post is None:
+                self.post = t.cuda.Stream(device=self.device)
+            self._stage(0, _native.STAGE_BIN | _native.STAGE_SCAN, main, None, frames_ptr)
+            if self._post_done is not None:
+                main.wait_event(self._post_done)
+            evs = None
+            if plane_events is not None:
+                e0, e1 = plane_events[0]
+                evs = [None, None, e0, e1]
+            self._stage(0, _native.STAGE_PLANES, main, evs, frames_ptr)
+            planed = t.cuda.Event()
+            planed.record(main)
+            self.post.wait_event(planed)
+            self._post(self.post, scores_ptr)
+            self._post_done = t.cuda.Event()
+            self._post_done.record(self.post)
+            return
+        self.join(main)
         if self.chunks == 1:
             evs = None
             if plane_events is not None:
@@ -259,6 +284,14 @@ class HogPipeline:
             main.wait_stream(post)
             return
         self._post(main, scores_ptr)
+
+    def join(self, stream=None):
+        """Make `stream` wait for the scores of the last pipelined run."""
+        if self._post_done is not None:
+            t = D.torch()
+            (stream if stream is not None else t.cuda.current_stream(self.device)).wait_event(
+                self._post_done)
+            self._post_done = None
 
     def run_staged(self, events, stream=None):
         """Diagnostic: the whole batch as one chunk with 4 recorded events

@@ -451,3 +451,30 @@ def test_band_rows_invariance(key, crop):
     lut = O.build_lut(cfg.bins)
     ref = O.integral_stack(O.gradient_map(frames[1], lut), cfg.bins)
     assert np.array_equal(outs[0][1][1].cpu().numpy().view(np.uint32), ref)
+
+
+def test_pipelined_batches_scores():
+    # consecutive pipelined runs: batch k's scores (post stream) overlap batch
+    # k+1's binning; batch k+1's plane kernel must wait for them (it rewrites
+    # the grid they read).  Alternate two batches with separate score buffers.
+    cfg = synth.CONFIGS["c4"]
+    n = 16
+    fa = synth.make_batch(cfg, 20, n)
+    fb = synth.make_batch(cfg, 40, n)
+    w, b = synth.make_weights(cfg)
+    p = H.HogPipeline(n, 3, cfg.height, cfg.width, cfg.bins, stride=cfg.stride, weights=w, bias=b)
+    outs = [torch.empty_like(p.scores) for _ in range(4)]
+    for i, fr in enumerate((fa, fb, fa, fb)):
+        p.upload(fr)
+        p.run(pipelined=True, scores_ptr=outs[i].data_ptr())
+    p.join()
+    torch.cuda.synchronize()
+    q = H.HogPipeline(n, 3, cfg.height, cfg.width, cfg.bins, stride=cfg.stride, weights=w, bias=b)
+    refs = []
+    for fr in (fa, fb):
+        q.upload(fr)
+        q.run()
+        torch.cuda.synchronize()
+        refs.append(q.scores.clone())
+    for i in range(4):
+        assert torch.equal(outs[i], refs[i % 2])
