@@ -8,15 +8,15 @@
 // relative tolerance allows (measured: ~1e-15).
 //
 // FP64-FMA-bound design (c5: 2304 FMAs per window, 3.7 G per frame):
-//   A warp owns SR_TY window rows x 32*TX window columns and streams the
-//   SR_TY + (cells_y-1)*K grid rows they read through its own two-slot ring
+//   A warp owns TY (4 or 5) window rows x 32*TX window columns and streams the
+//   TY + (cells_y-1)*K grid rows they read through its own two-slot ring
 //   in shared memory (no CTA-wide barrier, so warps never wait on rows they
 //   do not use).  Row r+1 is copied by cp.async (4-byte, zero-fill past the
 //   frame) while row r is consumed.  Slots are int32 [column/TX][column%TX][bin]
 //   with one pad word per TX columns: lane L reads column TX*L + j at word
 //   L*(TX*bins+1) + ..., an odd lane stride, so the reads are conflict-free.
 //   Per (row, bin) a lane converts its TX + 7K grid values to double once and
-//   reuses them for the SR_TY window rows that read that grid row (sr_row:
+//   reuses them for the TY window rows that read that grid row (sr_row:
 //   one unrolled body per active-row mask, so no FMA is spent on rows that
 //   do not read it); weights are warp-broadcast LDS.128.
 //
@@ -32,7 +32,18 @@
 
 namespace hogb200 {
 
-constexpr int SR_TY = 4, SR_WARPS = 4;
+constexpr int SR_WARPS = 4;  // window rows per warp: the template parameter TY (4 or 5)
+
+// Active-row masks a grid row can produce: for K = 1 a contiguous run of
+// bits, for K = 2 a contiguous run of one parity (bits p, p+2, ...).
+__host__ __device__ constexpr bool sr_mask_ok(int k, int m) {
+    if (m <= 0) return false;
+    while (!(m & 1)) m >>= 1;
+    if (k == 1) return (m & (m + 1)) == 0;
+    for (; m; m >>= 2)
+        if ((m & 3) != 1 && m != 1) return false;
+    return true;
+}
 
 __device__ __forceinline__ void cp_async4(uint32_t *sdst, const int32_t *gsrc, bool valid) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_addr(sdst)), "l"(gsrc),
@@ -61,14 +72,14 @@ __host__ __device__ inline int sr_slot_words(int bins, int tx, int k, bool u8 = 
 // Only active rows are computed: with a runtime zero-weight row instead, a
 // warp's 4 window rows would do 19 rows of FMAs for 16 useful ones (K = 1) or
 // twice the useful work (K = 2, where alternate rows are inactive).
-template <int K, int TX, int BINS, bool U8, int MASK>
-__device__ __forceinline__ void sr_row(double (&acc)[SR_TY][TX], const double *__restrict__ wsm,
+template <int K, int TX, int BINS, bool U8, int TY, int MASK>
+__device__ __forceinline__ void sr_row(double (&acc)[TY][TX], const double *__restrict__ wsm,
                                        int bins, int rr, const uint32_t *row, const uint8_t *rowb,
                                        int ctb) {
     constexpr int CX = 8, NG = TX / K + CX - 1;
-    const double *wu[SR_TY];
+    const double *wu[TY];
 #pragma unroll
-    for (int u = 0; u < SR_TY; ++u) wu[u] = wsm + ((MASK >> u) & 1 ? (rr - u) / K : 0) * bins * CX;
+    for (int u = 0; u < TY; ++u) wu[u] = wsm + ((MASK >> u) & 1 ? (rr - u) / K : 0) * bins * CX;
     for (int bn = 0; bn < bins; ++bn) {
 #pragma unroll
         for (int p = 0; p < K; ++p) {
@@ -83,12 +94,12 @@ __device__ __forceinline__ void sr_row(double (&acc)[SR_TY][TX], const double *_
             }
 #pragma unroll
             for (int cx = 0; cx < CX; cx += 2) {
-                double2 w2[SR_TY];
+                double2 w2[TY];
 #pragma unroll
-                for (int u = 0; u < SR_TY; ++u)
+                for (int u = 0; u < TY; ++u)
                     if ((MASK >> u) & 1) w2[u] = *reinterpret_cast<const double2 *>(wu[u] + bn * CX + cx);
 #pragma unroll
-                for (int u = 0; u < SR_TY; ++u)
+                for (int u = 0; u < TY; ++u)
                     if ((MASK >> u) & 1) {
 #pragma unroll
                         for (int t = 0; t < TX / K; ++t) {
@@ -101,9 +112,22 @@ __device__ __forceinline__ void sr_row(double (&acc)[SR_TY][TX], const double *_
     }
 }
 
+// if-chain over the masks valid for (K, TY): one unrolled sr_row per mask
+template <int K, int TX, int BINS, bool U8, int TY, int M = 1>
+__device__ __forceinline__ void sr_dispatch(int mask, double (&acc)[TY][TX],
+                                            const double *__restrict__ wsm, int bins, int rr,
+                                            const uint32_t *row, const uint8_t *rowb, int ctb) {
+    if constexpr (M < (1 << TY)) {
+        if constexpr (sr_mask_ok(K, M)) {
+            if (mask == M) return sr_row<K, TX, BINS, U8, TY, M>(acc, wsm, bins, rr, row, rowb, ctb);
+        }
+        sr_dispatch<K, TX, BINS, U8, TY, M + 1>(mask, acc, wsm, bins, rr, row, rowb, ctb);
+    }
+}
+
 // TX window columns per lane (32*TX per warp); BINS > 0: bin count known at
 // compile time (shared-memory offsets become immediates), 0: runtime `bins`.
-template <int K, int TX, int BINS, bool U8>
+template <int K, int TX, int BINS, bool U8, int TY>
 __global__ void __launch_bounds__(32 * SR_WARPS, 3)
 k_scores_rows(const void *__restrict__ grid_v, int n, int ncy, int ncx, int bins_rt, int noy,
               int nox, int cells_y, const double *__restrict__ wts, double bias,
@@ -121,14 +145,14 @@ k_scores_rows(const void *__restrict__ grid_v, int n, int ncy, int ncx, int bins
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t *ring = reinterpret_cast<uint32_t *>(ssm + (size_t)cells_y * bins * CX) + warp * 2 * slotw;
     const int tiles_x = (nox + COLS - 1) / COLS;
-    const int tiles_y = (noy + SR_TY * SR_WARPS - 1) / (SR_TY * SR_WARPS);
+    const int tiles_y = (noy + TY * SR_WARPS - 1) / (TY * SR_WARPS);
     int bid = blockIdx.x;
     const int tx = bid % tiles_x;
     bid /= tiles_x;
     const int ty = bid % tiles_y;
     const int f = bid / tiles_y;
     const int ix0 = tx * COLS;
-    const int iyw = ty * SR_TY * SR_WARPS + warp * SR_TY;  // this warp's first window row
+    const int iyw = ty * TY * SR_WARPS + warp * TY;  // this warp's first window row
     const T *gf = grid + (int64_t)f * ncy * ncx * bins;
     const int64_t gtotal = (int64_t)n * ncy * ncx * bins;  // grid elements (bytes if U8)
 
@@ -166,14 +190,14 @@ k_scores_rows(const void *__restrict__ grid_v, int n, int ncy, int ncx, int bins
         }
         cp_async_commit();
     };
-    double acc[SR_TY][TX];
+    double acc[TY][TX];
 #pragma unroll
-    for (int u = 0; u < SR_TY; ++u)
+    for (int u = 0; u < TY; ++u)
 #pragma unroll
         for (int t = 0; t < TX; ++t) acc[u][t] = 0.0;
 
     const int r_first = iyw;
-    const int r_last = min(iyw + SR_TY - 1, noy - 1) + (cells_y - 1) * K;
+    const int r_last = min(iyw + TY - 1, noy - 1) + (cells_y - 1) * K;
     stage(r_first, ring);
     // lane L's columns start at TX*L, the first column of chunk L: lane stride TX*bins+1 (odd)
     const int c0 = TX * lane;
@@ -194,40 +218,14 @@ k_scores_rows(const void *__restrict__ grid_v, int n, int ncy, int ncx, int bins
         const int rr = r - iyw;
         int mask = 0;
 #pragma unroll
-        for (int u = 0; u < SR_TY; ++u) {
+        for (int u = 0; u < TY; ++u) {
             const int d = rr - u;
             if (d >= 0 && d % K == 0 && d / K < cells_y) mask |= 1 << u;
         }
-#define SR_ROW(M) sr_row<K, TX, BINS, U8, M>(acc, wsm, bins, rr, row, rowb, ctb)
-        if constexpr (K == 1) {
-            switch (mask) {
-                case 15: SR_ROW(15); break;
-                case 1: SR_ROW(1); break;
-                case 3: SR_ROW(3); break;
-                case 7: SR_ROW(7); break;
-                case 14: SR_ROW(14); break;
-                case 12: SR_ROW(12); break;
-                case 8: SR_ROW(8); break;
-                case 2: SR_ROW(2); break;  // runs of length 1-2 in the middle: cells_y < 4
-                case 4: SR_ROW(4); break;
-                case 6: SR_ROW(6); break;
-                default: break;  // masks are contiguous runs of bits: all listed
-            }
-        } else {
-            switch (mask) {
-                case 5: SR_ROW(5); break;
-                case 10: SR_ROW(10); break;
-                case 1: SR_ROW(1); break;
-                case 2: SR_ROW(2); break;
-                case 4: SR_ROW(4); break;
-                case 8: SR_ROW(8); break;
-                default: break;  // masks are runs of one parity: all listed
-            }
-        }
-#undef SR_ROW
+sr_dispatch<K, TX, BINS, U8, TY>(mask, acc, wsm, bins, rr, row, rowb, ctb);
     }
 #pragma unroll
-    for (int u = 0; u < SR_TY; ++u) {
+    for (int u = 0; u < TY; ++u) {
         const int iy = iyw + u;
         if (iy >= noy) continue;
         double *sp = scores + ((int64_t)f * noy + iy) * nox + ix0 + c0;
@@ -242,20 +240,62 @@ size_t scores_rows_smem(int bins, int cells_y, int tx, int k, bool u8) {
            sizeof(uint32_t) * (size_t)SR_WARPS * 2 * sr_slot_words(bins, tx, k, u8);
 }
 
-template <int K, int TX, int BINS, bool U8>
-void launch_rows_t(const void *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
-                   int cells_y, const double *wts, double bias, double *scores, cudaStream_t st) {
+template <int K, int TX, int BINS, bool U8, int TY>
+void launch_rows_ty(const void *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
+                    int cells_y, const double *wts, double bias, double *scores, cudaStream_t st) {
     const size_t smem = scores_rows_smem(bins, cells_y, TX, K, U8);
     static size_t configured[HOG_MAX_DEVICES] = {};
     if (smem_optin_needed(configured, smem))
-        cudaFuncSetAttribute(k_scores_rows<K, TX, BINS, U8>,
+        cudaFuncSetAttribute(k_scores_rows<K, TX, BINS, U8, TY>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // e / (TX bins) by multiply-high: exact for e < 2^20 (e < span * bins here)
     const uint32_t magic = (uint32_t)((0x100000000ull + TX * bins - 1) / (TX * bins));
-    const int64_t blocks = (int64_t)n * ((noy + SR_TY * SR_WARPS - 1) / (SR_TY * SR_WARPS)) *
+    const int64_t blocks = (int64_t)n * ((noy + TY * SR_WARPS - 1) / (TY * SR_WARPS)) *
                            ((nox + 32 * TX - 1) / (32 * TX));
-    k_scores_rows<K, TX, BINS, U8><<<(unsigned)blocks, 32 * SR_WARPS, smem, st>>>(
+    k_scores_rows<K, TX, BINS, U8, TY><<<(unsigned)blocks, 32 * SR_WARPS, smem, st>>>(
         grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias, scores, magic);
+}
+
+// Window rows per warp: 5 instead of 4 when that takes fewer CTA waves of the
+// same occupancy, by the model time ~ waves x (FMA rows + 0.3 x staged rows)
+// of a task.  c4 (75 window rows x 256 frames, 4 CTAs/SM): 2.16 -> 1.73
+// waves.  Only for the byte grid at stride = cell (K = 1).
+template <int K, int TX, int BINS, bool U8>
+void launch_rows_t(const void *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
+                   int cells_y, const double *wts, double bias, double *scores, cudaStream_t st) {
+    if constexpr (U8 && K == 1) {
+        const char *e = getenv("HOGB200_SCORES_TY");
+        int ty = e ? atoi(e) : 0;
+        if (ty != 4 && ty != 5) {
+            const int tiles_x = (nox + 32 * TX - 1) / (32 * TX);
+            double cost[2];
+            for (int i = 0; i < 2; ++i) {
+                const int t = 4 + i;
+                const size_t smem = scores_rows_smem(bins, cells_y, TX, K, U8);
+                int per_sm = 0;
+                if (t == 4)
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                        &per_sm, k_scores_rows<K, TX, BINS, U8, 4>, 32 * SR_WARPS, smem);
+                else
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                        &per_sm, k_scores_rows<K, TX, BINS, U8, 5>, 32 * SR_WARPS, smem);
+                int sms = 148;
+                int dev = 0;
+                if (cudaGetDevice(&dev) == cudaSuccess)
+                    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                const int64_t blocks = (int64_t)n * tiles_x * ((noy + t * SR_WARPS - 1) / (t * SR_WARPS));
+                const int64_t slots = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+                const double waves = (double)((blocks + slots - 1) / slots);
+                cost[i] = waves * (t * cells_y + 0.3 * (t + cells_y - 1));
+            }
+            ty = cost[1] < 0.97 * cost[0] ? 5 : 4;
+        }
+        if (ty == 5)
+            return launch_rows_ty<K, TX, BINS, U8, 5>(grid, n, ncy, ncx, bins, noy, nox, cells_y,
+                                                      wts, bias, scores, st);
+    }
+    launch_rows_ty<K, TX, BINS, U8, 4>(grid, n, ncy, ncx, bins, noy, nox, cells_y, wts, bias,
+                                       scores, st);
 }
 
 template <int K, int TX, bool U8>

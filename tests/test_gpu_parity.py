@@ -478,3 +478,27 @@ def test_pipelined_batches_scores():
         refs.append(q.scores.clone())
     for i in range(4):
         assert torch.equal(outs[i], refs[i % 2])
+
+
+@pytest.mark.parametrize("bins,h,w,wh", [(8, 300, 700, 128), (18, 250, 1000, 128), (9, 180, 400, 40)])
+def test_scores_rows_five_rows_per_warp(monkeypatch, bins, h, w, wh):
+    # 5 window rows per warp (chosen when it saves a CTA wave, c4) against 4
+    # and the oracle; window-row counts that are not multiples of 5 or 20
+    rng = np.random.default_rng(bins + h)
+    frames = rng.integers(0, 256, (3, 1, h, w), dtype=np.uint8)
+    cells_y = wh // 8
+    wts = rng.normal(0, 0.01, 8 * cells_y * bins)
+    got = []
+    for ty in ("4", "5"):
+        monkeypatch.setenv("HOGB200_SCORES_TY", ty)
+        p = H.HogPipeline(3, 1, h, w, bins, stride=8, window=(64, wh), weights=wts, bias=0.3)
+        p.upload(frames)
+        p.run()
+        torch.cuda.synchronize()
+        got.append(p.scores.cpu().numpy())
+    np.testing.assert_allclose(got[0], got[1], rtol=1e-12, atol=score_tol(wts))
+    g = O.Geometry(64, wh, 8, 1, 1, bins)
+    lut = O.build_lut(bins)
+    for i in (0, 2):
+        ref = O.scan_scores(O.integral_stack(O.gradient_map(frames[i], lut), bins), g, 8, wts, 0.3)
+        np.testing.assert_allclose(got[1][i], ref, rtol=1e-9, atol=score_tol(wts))
