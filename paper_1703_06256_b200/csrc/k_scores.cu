@@ -167,17 +167,19 @@ k_scores_rows(const void *__restrict__ grid_v, int n, int ncy, int ncx, int bins
     const int ctb = TX * bins;  // words of a chunk of TX columns (+1 pad word)
     auto stage = [&](int r, uint32_t *dst) {  // async copy of grid row r (this warp's columns)
         if constexpr (U8) {
-            // bytes [a0, a0 + 16*nch) of the whole grid, a0 the 16-byte boundary at or below
-            // the row start; values past the frame's right edge only feed window columns
-            // that are not stored
-            const int64_t b0 = (((int64_t)f * ncy + r) * ncx + ix0) * bins;
-            const int64_t a0 = b0 & ~(int64_t)15;
-            const int nch = (int)((b0 - a0) + SPAN * bins + 15) / 16;
+            // the 16-byte-aligned ADDRESSES at or below the row start (the grid pointer
+            // itself may be unaligned: a frame group's slice of a batch grid); zero-fill
+            // past the end of the grid; values past the frame's right edge only feed
+            // window columns that are not stored
+            const uintptr_t a = reinterpret_cast<uintptr_t>(grid) +
+                                (uintptr_t)((((int64_t)f * ncy + r) * ncx + ix0) * bins);
+            const uintptr_t a0 = a & ~(uintptr_t)15;
+            const uintptr_t end = reinterpret_cast<uintptr_t>(grid) + (uintptr_t)gtotal;
+            const int nch = (int)((a - a0) + SPAN * bins + 15) / 16;
             for (int e = lane; e < nch; e += 32) {
-                const int64_t o = a0 + 16 * (int64_t)e;
-                const int64_t left = gtotal - o;
-                const int bytes = left >= 16 ? 16 : (left > 0 ? (int)left : 0);
-                cp_async16(dst + 4 * e, bytes ? grid + o : grid, bytes);
+                const uintptr_t o = a0 + 16 * (uintptr_t)e;
+                const int bytes = o + 16 <= end ? 16 : (o < end ? (int)(end - o) : 0);
+                cp_async16(dst + 4 * e, reinterpret_cast<const void *>(bytes ? o : a0), bytes);
             }
         } else {
             const int32_t *src = gf + ((int64_t)r * ncx + ix0) * bins;
@@ -210,8 +212,9 @@ k_scores_rows(const void *__restrict__ grid_v, int n, int ncy, int ncx, int bins
         const uint32_t *row = ring + slot * slotw + lbase;
         const uint8_t *rowb = nullptr;
         if constexpr (U8) {
-            const int64_t b0 = (((int64_t)f * ncy + r) * ncx + ix0) * bins;
-            rowb = reinterpret_cast<const uint8_t *>(ring + slot * slotw) + (int)(b0 & 15) +
+            const uintptr_t a = reinterpret_cast<uintptr_t>(grid) +
+                                (uintptr_t)((((int64_t)f * ncy + r) * ncx + ix0) * bins);
+            rowb = reinterpret_cast<const uint8_t *>(ring + slot * slotw) + (int)(a & 15) +
                    c0 * bins;
         }
         // window rows reading grid row r: u with d = rr - u in [0, (cells_y-1)*K], d % K == 0

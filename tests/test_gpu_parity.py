@@ -359,16 +359,18 @@ def test_scores_rows_kernel(monkeypatch, bins, stride, h, w):
         np.testing.assert_allclose(got[0][i], ref, rtol=1e-9, atol=score_tol(wts))
 
 
-@pytest.mark.parametrize("chunks", [2, 3])
-def test_chunked_two_stream_pipeline_matches(chunks):
+@pytest.mark.parametrize("chunks,h,w", [(2, 200, 320), (3, 200, 320), (3, 140, 330)])
+def test_chunked_two_stream_pipeline_matches(chunks, h, w):
     # frame groups on two streams (binning of group j+1 under the planes of
-    # group j) give the same bin maps, planes, grid and scores as one launch
+    # group j) give the same bin maps, planes, grid and scores as one launch;
+    # at 140 x 330 a frame's byte grid is 5,576 bytes, so the groups' grid
+    # slices start off 16-byte boundaries (the score kernel's staging copies)
     cfg = synth.CONFIGS["c4"]
-    frames = np.ascontiguousarray(synth.make_batch(cfg, 7, 5)[:, :, :200, :320])
-    w, b = synth.make_weights(cfg)
+    frames = np.ascontiguousarray(synth.make_batch(cfg, 7, 5)[:, :, :h, :w])
+    w_, b = synth.make_weights(cfg)
     outs = []
     for ch in (1, chunks):
-        p = H.HogPipeline(5, 3, 200, 320, cfg.bins, stride=cfg.stride, weights=w, bias=b, chunks=ch)
+        p = H.HogPipeline(5, 3, h, w, cfg.bins, stride=cfg.stride, weights=w_, bias=b, chunks=ch)
         assert p.chunks == ch
         p.upload(frames)
         p.run()

@@ -93,7 +93,7 @@ ref = H.nms(H.pyramid_scan(H.Image(fr[0]), model, 1.2, 8, 0.0), 0.5)
 check("pyramid detections + NMS", [(x.x, x.y, x.w, x.h) for x in dets] == [(x.x, x.y, x.w, x.h) for x in ref])
 
 # 5. 16-bit planes and batched rectangle queries
-small = np.ascontiguousarray(fr[:, :120, :150])
+small = np.ascontiguousarray(fr[0, :, :120, :150])
 st16 = H.build_integral_stack(H.gradient_map(H.Image(small), H.build_lut(8)), acc_width=16)
 ref16 = O.integral_stack(O.gradient_map(small, O.build_lut(8)), 8).astype(np.uint16)
 check("integral16", np.array_equal(np.asarray(st16.planes), ref16))
