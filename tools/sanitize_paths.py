@@ -8,6 +8,11 @@ oracle, so the sanitizer sees the real code paths), then e.g.
     compute-sanitizer --tool synccheck python tools/sanitize_paths.py
 
 Band-row tuning is off (HOGB200_TUNE=0): it times kernels on unwritten frames.
+
+On this round's GPU pool compute-sanitizer is closed by the operators (it left
+GPUs needing a reset; profiles/r1b_compute_sanitizer_unavailable.txt), so the
+bare run -- every entry point at small, misaligned and ragged sizes against
+the oracle (profiles/r1b_all_paths_small_vs_oracle.txt) -- is the check.
 """
 import os
 import sys
