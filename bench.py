@@ -359,9 +359,11 @@ def main():
     barrier()
     torch.cuda.synchronize()
     sampler.start()
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/": the timed kernels only
     start.record()
     launch()
     end.record()
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     clocks = sampler.stop()
     barrier()
@@ -480,10 +482,12 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
     barrier()
     torch.cuda.synchronize()
     sampler.start()
+    torch.cuda.nvtx.range_push("timed")
     start.record()
     for _ in range(K):
         p.run(plane_events=pev)
     end.record()
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     clocks = sampler.stop()
     barrier()
