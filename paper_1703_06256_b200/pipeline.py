@@ -298,6 +298,7 @@ class HogPipeline:
         bracketing binning, carry scan and planes (+ grid)."""
         t = D.torch()
         main = stream if stream is not None else t.cuda.current_stream(self.device)
+        self.join(main)
         saved = self.ranges, self.scratch
         if self.chunks > 1:  # one chunk needs the whole-batch scratch
             sb = int(_native.load().hog_scratch_bytes(self.n, self.h, self.w, self.bins,
@@ -358,6 +359,7 @@ class HogPipeline:
 
         if self.scores is None:
             raise ValueError("detections need a pipeline built with weights")
+        self.join()
         g = self.geometry
         ww, wh = DT.window_box_size(g.window_w, g.window_h, scale)
         boxes, sc, _, counts = DT.compact(self.scores, self.oxs, self.oys, threshold, scale, ww, wh)
