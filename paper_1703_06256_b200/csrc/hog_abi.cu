@@ -95,6 +95,9 @@ TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int ce
     const int maxw = k2_maxt(g.NW, g.VC) / 32 - (tma ? 1 : 0);
     g.NWARP = g.ns < maxw ? g.ns : maxw;
     g.nss = (g.ns + g.NWARP - 1) / g.NWARP;
+    // spread the strips evenly over the super-strips: the last super-strip of a
+    // band otherwise runs with idle warps (8K pyramid level 5: 25 strips as 6+6+6+6+1)
+    if (env_int("HOGB200_BALANCE_STRIPS", 1)) g.NWARP = (g.ns + g.nss - 1) / g.nss;
     g.nc1 = (w + CHUNK - 1) / CHUNK;
     g.Wc = g.nc1 * CHUNK;
     int R = 128;
