@@ -220,27 +220,40 @@ __global__ void k_scan_cols(TileGeom g, Scratch sc) {
             run[w] = lo | (hi << 16);
         }
     }
-    // C and V never alias: read-only loads that the compiler may hoist ahead
-    // of the V stores, so several bands' loads are in flight
+    // C and V never alias.  The sub-band counts are loaded 8 at a time, all
+    // issued before any is used, so a column's chain over the bands waits on
+    // one memory latency per 8 sub-bands (a single small frame -- config c1 --
+    // spent 18 us here with one dependent load per sub-band)
     const uint32_t *__restrict__ Cf = sc.C + (int64_t)f * g.nb1 * g.Wc * NWB + (int64_t)x * NWB;
     uint32_t *__restrict__ Vf = sc.V + (int64_t)f * g.nb2 * g.Wc * g.NWp + (int64_t)x * g.NWp;
-#pragma unroll 4
-    for (int b = 0; b < g.nb2; ++b) {
+    auto store_v = [&](int b) {
         uint4 *vp = reinterpret_cast<uint4 *>(Vf + (int64_t)b * g.Wc * g.NWp);
 #pragma unroll
         for (int q = 0; q < (NW + 3) / 4; ++q)  // 16-B stores; words past NW are zero padding
             vp[q] = make_uint4(run[4 * q], 4 * q + 1 < NW ? run[4 * q + 1] : 0u,
                                4 * q + 2 < NW ? run[4 * q + 2] : 0u, 4 * q + 3 < NW ? run[4 * q + 3] : 0u);
-        // plane band b covers pixel sub-bands [b*S1, (b+1)*S1)
-        for (int s = b * g.S1; s < min((b + 1) * g.S1, g.nb1); ++s) {
-            const uint32_t *cp = Cf + (int64_t)s * g.Wc * NWB;
-            uint32_t c8[NWB];
+    };
+    constexpr int SB = 8;
+    int nextb = 0, nexts = 0;  // next plane band whose carry is due, and its first sub-band
+    for (int s0 = 0; s0 < g.nb1; s0 += SB) {
+        uint32_t c8[SB][NWB];
 #pragma unroll
-            for (int w = 0; w < NWB; ++w) c8[w] = __ldg(cp + w);
+        for (int i = 0; i < SB; ++i)
 #pragma unroll
-            for (int w = 0; w < NW; ++w) run[w] += widen_half(c8[w >> 1], w & 1);
+            for (int w = 0; w < NWB; ++w)
+                c8[i][w] = s0 + i < g.nb1 ? __ldg(Cf + (int64_t)(s0 + i) * g.Wc * NWB + w) : 0u;
+#pragma unroll
+        for (int i = 0; i < SB; ++i) {
+            const int s = s0 + i;
+            if (s == nexts && nextb < g.nb2) {  // plane band nextb covers sub-bands from s on
+                store_v(nextb++);
+                nexts += g.S1;
+            }
+#pragma unroll
+            for (int w = 0; w < NW; ++w) run[w] += widen_half(c8[i][w >> 1], w & 1);
         }
     }
+    for (; nextb < g.nb2; ++nextb) store_v(nextb);  // bands starting at or past the last row
 }
 
 template <int NWB>
