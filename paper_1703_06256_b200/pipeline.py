@@ -472,8 +472,10 @@ class PyramidPipeline:
         if streams is None:
             import os
 
-            # measured on B200 (c5, 32 x 8K): 1 stream 85.1 ms, 2: 76.6, 3: 75.7
-            streams = int(os.environ.get("HOGB200_PYR_STREAMS", "3"))
+            # measured on B200 (c5, 32 x 8K): 1 stream 85.1 ms, 2: 76.6, 3: 75.7; with
+            # the byte-grid scores, 2: 68.9, 3: 68.3, 4: 67.9, 6: 67.7
+            # (profiles/r1b_c5_schedule_sweep.txt)
+            streams = int(os.environ.get("HOGB200_PYR_STREAMS", "4"))
         self.streams = max(1, min(int(streams), len(self.levels)))
         self._side = [t.cuda.Stream(device=self.device) for _ in range(self.streams - 1)]
 
