@@ -54,6 +54,8 @@ def parse_args():
                     help="e2e: split the last chunk in this many pieces (shorter drain)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the timed steps (and the e2e step) eagerly, no CUDA graph")
+    ap.add_argument("--e2e-overlap", type=int, default=1,
+                    help="e2e: step k+1's first copies start while step k's last chunks drain")
     ap.add_argument("--pipelined", type=int, default=1,
                     help="scored configs: batch k's scores run beside batch k+1's binning")
     ap.add_argument("--pyr-streams", type=int, default=0,
@@ -395,7 +397,8 @@ def main():
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier,
-                      args.e2e_chunk, args.e2e_slots, not args.no_graph, args.e2e_tail)
+                      args.e2e_chunk, args.e2e_slots, not args.no_graph, args.e2e_tail,
+                      bool(args.e2e_overlap))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -621,7 +624,7 @@ def run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrie
 
 
 def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, chunk=64, nslots=2,
-            use_graph=True, tail=1):
+            use_graph=True, tail=1, overlap=True):
     """Per step: H2D of every frame from pinned host memory, the pipeline, and
     D2H of the step's result, in frame chunks.  Each direction has ONE copy
     stream, so chunks cross PCIe in order at full bandwidth (copies issued on
@@ -661,53 +664,64 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
     res = jobs[0][2].result()
     host_out = torch.empty((nf,) + tuple(res.shape[1:]), dtype=res.dtype).pin_memory()
 
-    def step():
+    def steps(nsteps):
+        """nsteps e2e steps.  Buffer reuse is guarded per pipeline (frames buffer
+        free once its last chunk is computed, result buffer free once that
+        result has left), so with overlap=True step k+1's first H2D copies
+        start while step k's last chunks are still computing / leaving; the
+        streams join the caller's stream only around the whole run."""
         cur = torch.cuda.current_stream()
         for st in (h2d, comp, d2h):
             st.wait_stream(cur)
-        landed, computed, left = [], [], []
-        for j, (a, b, q) in enumerate(jobs):
-            landed.append(torch.cuda.Event())
-            computed.append(torch.cuda.Event())
-            left.append(torch.cuda.Event())
-            if j >= nslots:
-                h2d.wait_event(computed[j - nslots])  # frames buffer free
-            with torch.cuda.stream(h2d):
-                dst = q.frames.data if q.frames.pitch == cfg.width else q.frames.data[..., : cfg.width]
-                dst.copy_(host_in[a:b], non_blocking=True)
-                landed[j].record(h2d)
-            comp.wait_event(landed[j])
-            if j >= nslots:
-                comp.wait_event(left[j - nslots])  # result buffer free
-            q.run(stream=comp)
-            computed[j].record(comp)
-            d2h.wait_event(computed[j])
-            with torch.cuda.stream(d2h):
-                host_out[a:b].copy_(q.result(), non_blocking=True)
-                left[j].record(d2h)
+        last = {}  # pipeline -> (computed, left) events of its latest chunk
+        for _ in range(nsteps):
+            for a, b, q in jobs:
+                prev = last.get(id(q))
+                if prev is not None:
+                    h2d.wait_event(prev[0])  # frames buffer free
+                with torch.cuda.stream(h2d):
+                    dst = q.frames.data if q.frames.pitch == cfg.width else q.frames.data[..., : cfg.width]
+                    dst.copy_(host_in[a:b], non_blocking=True)
+                    landed = torch.cuda.Event()
+                    landed.record(h2d)
+                comp.wait_event(landed)
+                if prev is not None:
+                    comp.wait_event(prev[1])  # result buffer free
+                q.run(stream=comp)
+                computed = torch.cuda.Event()
+                computed.record(comp)
+                d2h.wait_event(computed)
+                with torch.cuda.stream(d2h):
+                    host_out[a:b].copy_(q.result(), non_blocking=True)
+                    left = torch.cuda.Event()
+                    left.record(d2h)
+                last[id(q)] = (computed, left)
+            if not overlap:
+                for st in (h2d, comp, d2h):
+                    cur.wait_stream(st)
+                for st in (h2d, comp, d2h):
+                    st.wait_stream(cur)
+                last.clear()
         for st in (h2d, comp, d2h):
             cur.wait_stream(st)
 
-    for _ in range(W):
-        step()
+    steps(W)
     torch.cuda.synchronize()
-    replay = step
+    replay = lambda: steps(K)  # noqa: E731
     if use_graph:
-        # the whole step (H2D copies, kernels, D2H copies on their streams)
+        # the K timed steps (H2D copies, kernels, D2H copies on their streams)
         # as one CUDA graph: no per-chunk host launch cost inside the timed loop
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            step()
+            steps(K)
         torch.cuda.synchronize()
         replay = g.replay
-        for _ in range(W):
-            replay()
+        replay()
         torch.cuda.synchronize()
     barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
-    for _ in range(K):
-        replay()
+    replay()
     t1.record()
     torch.cuda.synchronize()
     ms = max_over_ranks([t0.elapsed_time(t1) / K])[0]
@@ -719,6 +733,7 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
             "result": "cell grid" if not cfg.scored else "window scores",
             "chunk_frames": sizes, "buffer_sets": nslots,
             "streams": "1 H2D + 1 compute + 1 D2H (in-order copies)", "cuda_graph": bool(use_graph),
+            "steps_overlap": bool(overlap),
             "matches_device_run": ok}
 
 
