@@ -92,7 +92,11 @@ TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int ce
     // (profiles/r1_tma_store_ab.md).  Pure stores do reach 7.2 TB/s this way
     // (tools/probe_tma_store.cu) against 5.5 TB/s for st.global.
     tma = tma && env_int("HOGB200_TMA", 0) != 0;
-    const int maxw = k2_maxt(g.NW, g.VC) / 32 - (tma ? 1 : 0);
+    // top row in registers when a band's strips fit the 6-warp variant (c2: 6
+    // strips; measured 1.153 -> 1.136 ms); wider small-bin frames keep 8 warps
+    g.PREG = (K2_PTOP_REG && 2 * g.NW * g.VC <= 32 && !tma && g.ns <= 6 &&
+              env_int("HOGB200_PTOP_REG", 1)) ? 1 : 0;
+    const int maxw = k2_maxt(g.NW, g.VC, g.PREG != 0) / 32 - (tma ? 1 : 0);
     g.NWARP = g.ns < maxw ? g.ns : maxw;
     g.nss = (g.ns + g.NWARP - 1) / g.NWARP;
     // spread the strips evenly over the super-strips: the last super-strip of a

@@ -46,6 +46,7 @@ struct TileGeom {
     int nss;    // super-strips: ceil(ns / NWARP)
     int ht, hb; // slab mode: the frame continues above row 0 / below row h-1 (rows -1 / h are
                 // readable halo rows, and rows 0 / h-1 are binned rather than border NO_BIN)
+    int PREG;   // k_planes keeps the band's top row in registers (k2_maxt preg variant)
     int TMA;    // plane rows staged in shared memory and written by TMA bulk stores
     int RING;   // TMA: staged plane rows in flight (ring slots)
     int SEGW;   // TMA: staged columns per bin row = NWARP*Ws + 8 (32-B aligned front pad)
@@ -101,7 +102,16 @@ constexpr int K2_G = 4;  // rows per phase-A/phase-B group
 // 8-column-per-lane and >= 10-bin variants spill at 128 registers and run
 // 4-29 % faster with 168 (c3, c4, c5); the c2 variant (4 columns, 8 bins) is
 // 4 % faster at 128.
-__host__ __device__ constexpr int k2_maxt(int nw, int vc) { return (vc == 8 || nw >= 5) ? 192 : 256; }
+#ifndef K2_PTOP_REG
+#define K2_PTOP_REG 1
+#endif
+// Plane-kernel CTA size bound.  preg: the small variants (<= 8 bins, 4 columns
+// per lane) keep the band's top row in 32 registers instead of shared memory,
+// bounded at 192 threads (170 registers at 2 CTAs/SM); chosen when a band's
+// strips fit 6 warps (make_geom), else the 256-thread variant runs.
+__host__ __device__ constexpr int k2_maxt(int nw, int vc, bool preg = false) {
+    return (vc == 8 || nw >= 5 || preg) ? 192 : 256;
+}
 
 // Inputs of the fused plane kernel (binning inside k_planes, band carries by
 // decoupled look-back instead of k_grad_bin counts + k_scan_cols).

@@ -181,13 +181,17 @@ __device__ __forceinline__ void bin_rows(const FusedIn &fi, const TileGeom &g, i
 // cp.async.bulk per (bin, row) -- whole 32-B sectors, no LSU traffic -- then
 // releases the slot on empty[slot] once the TMA engine has read it.  The
 // compute warps synchronise among themselves with named barrier 1.
-template <int NW, int KR, int VC, bool VEC, int CH = 0, bool TMA = false>
-__global__ void __launch_bounds__(k2_maxt(NW, VC), K2_MINB)
+template <int NW, int KR, int VC, bool VEC, int CH = 0, bool TMA = false, bool PR = false>
+__global__ void __launch_bounds__(k2_maxt(NW, VC, PR), K2_MINB)
 k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, GridOut go,
          TileGeom g, Scratch sc, FusedIn fi) {
     extern __shared__ __align__(16) uint32_t smem[];
     constexpr int NB = 2 * NW;
     constexpr int NWB = (NB + 3) / 4;
+    // the band's top row in registers (small variants): no shared-memory load per
+    // stored value (c2: 8 LDS.128 per row and lane, a short-scoreboard stall each)
+    constexpr bool PREG = PR && NB * VC <= 32 && !TMA;
+    uint32_t preg[PREG ? NB : 1][PREG ? VC : 1];
     constexpr int G = K2_G;
     const int nwarp = g.NWARP;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -393,10 +397,15 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                     uint32_t pt[VC];
 #pragma unroll
                     for (int k = 0; k < VC; ++k) pt[k] = (run += half16(v[k], h));
+                    if constexpr (PREG) {
 #pragma unroll
-                    for (int k = 0; k < VC; k += 4)
-                        *reinterpret_cast<uint4 *>(ptop + n * 32 * VC + k) =
-                            make_uint4(pt[k], pt[k + 1], pt[k + 2], pt[k + 3]);
+                        for (int k = 0; k < VC; ++k) preg[PREG ? n : 0][PREG ? k : 0] = pt[k];
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < VC; k += 4)
+                            *reinterpret_cast<uint4 *>(ptop + n * 32 * VC + k) =
+                                make_uint4(pt[k], pt[k + 1], pt[k + 2], pt[k + 3]);
+                    }
                     const uint32_t stot = __shfl_sync(FULL, inc, lo);  // strip total (own lanes)
                     if (lane == 0) vtot[warp * NB + n] = stot;
                 }
@@ -474,13 +483,18 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                 for (int n = 0; n < NB; ++n) {
                     if (n < NB - 1 || !odd) {
                         uint32_t vals[VC];
+                        if constexpr (PREG) {
 #pragma unroll
-                        for (int k = 0; k < VC; k += 4) {
-                            const uint4 t4 = *reinterpret_cast<const uint4 *>(ptop + n * 32 * VC + k);
-                            vals[k] = t4.x;
-                            vals[k + 1] = t4.y;
-                            vals[k + 2] = t4.z;
-                            vals[k + 3] = t4.w;
+                            for (int k = 0; k < VC; ++k) vals[k] = preg[PREG ? n : 0][PREG ? k : 0];
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < VC; k += 4) {
+                                const uint4 t4 = *reinterpret_cast<const uint4 *>(ptop + n * 32 * VC + k);
+                                vals[k] = t4.x;
+                                vals[k + 1] = t4.y;
+                                vals[k + 2] = t4.z;
+                                vals[k + 3] = t4.w;
+                            }
                         }
 #pragma unroll
                         for (int k = 0; k < VC; ++k) vals[k] += Lacc[n] + half16(Q[n >> 1][k], n & 1);
@@ -502,7 +516,8 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
             uint32_t gv[NB];
 #pragma unroll
             for (int n = 0; n < NB; ++n) {
-                const uint32_t lv = ptop[n * 32 * VC + VC - 1] + Lacc[n] + half16(Q[n >> 1][VC - 1], n & 1);
+                const uint32_t pt_last = PREG ? preg[PREG ? n : 0][PREG ? VC - 1 : 0] : ptop[n * 32 * VC + VC - 1];
+                const uint32_t lv = pt_last + Lacc[n] + half16(Q[n >> 1][VC - 1], n & 1);
                 const uint32_t r = __shfl_down_sync(FULL, lv, dR);
                 uint32_t l = __shfl_up_sync(FULL, lv, 1);
                 if (lane == 0) l = Lacc[n];
@@ -700,16 +715,16 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
     }
 }
 
-template <int NW, int KR, int VC, bool VEC, int CH, bool TMA = false>
+template <int NW, int KR, int VC, bool VEC, int CH, bool TMA = false, bool PR = false>
 void launch_planes_vc(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
                       const GridOut &go, const TileGeom &g, const Scratch &sc, const FusedIn &fi,
                       cudaStream_t st) {
     const size_t smem = (size_t)k2_smem_words(g, KR) * 4;
     static size_t configured[HOG_MAX_DEVICES] = {};  // per instantiation and device
     if (smem_optin_needed(configured, smem))
-        cudaFuncSetAttribute(k_planes<NW, KR, VC, VEC, CH, TMA>,
+        cudaFuncSetAttribute(k_planes<NW, KR, VC, VEC, CH, TMA, PR>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_planes<NW, KR, VC, VEC, CH, TMA>
+    k_planes<NW, KR, VC, VEC, CH, TMA, PR>
         <<<(unsigned)((int64_t)g.n * g.nb2), 32 * (g.NWARP + (TMA ? 1 : 0)), smem, st>>>(
             bm, bp, bfs, po, go, g, sc, fi);
 }
@@ -738,6 +753,13 @@ void launch_planes_kr(int ch, const int8_t *bm, int64_t bp, int64_t bfs, const P
     }
     if constexpr (NW <= 5) {
         if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 0>(bm, bp, bfs, po, go, g, sc, fi, st);
+    }
+    if constexpr (2 * NW * 4 <= 32) {
+        if (g.PREG) {
+            if (po.vec)
+                return launch_planes_vc<NW, KR, 4, true, 0, false, true>(bm, bp, bfs, po, go, g, sc, fi, st);
+            return launch_planes_vc<NW, KR, 4, false, 0, false, true>(bm, bp, bfs, po, go, g, sc, fi, st);
+        }
     }
     if (po.vec)
         launch_planes_vc<NW, KR, 4, true, 0>(bm, bp, bfs, po, go, g, sc, fi, st);
