@@ -504,3 +504,32 @@ def test_scores_rows_five_rows_per_warp(monkeypatch, bins, h, w, wh):
     for i in (0, 2):
         ref = O.scan_scores(O.integral_stack(O.gradient_map(frames[i], lut), bins), g, 8, wts, 0.3)
         np.testing.assert_allclose(got[1][i], ref, rtol=1e-9, atol=score_tol(wts))
+
+
+@pytest.mark.parametrize("key,count", [("c4", 80), ("c2", 256)])
+def test_big_batch_paths_vs_oracle(key, count):
+    # the variants only big batches select (>= 64 Mpx: 8 plane columns per
+    # lane with 256-bit stores for c4; band rows / sub-bands sized for many
+    # CTAs): first and last frame against the oracle, scores of both
+    cfg = synth.CONFIGS[key]
+    frames = synth.make_batch(cfg, 100, count)
+    weights, bias = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
+    p = H.HogPipeline(count, cfg.channels, cfg.height, cfg.width, cfg.bins, stride=cfg.stride,
+                      weights=weights, bias=bias)
+    p.upload(frames)
+    p.run()
+    torch.cuda.synchronize()
+    lut = O.build_lut(cfg.bins)
+    ends = [0, count - 1]
+    mode = 1 if cfg.scored else 0
+    _, grid, scores = O.run_batch(frames[ends], lut, cfg.bins, 8, 64, 128, cfg.stride, mode,
+                                  weights, bias, threads=4, want_outputs=True)
+    assert np.array_equal(p.grid[ends].cpu().numpy().astype(np.int64), grid)
+    for i in ends:
+        cells = O.gradient_map(frames[i], lut)
+        assert np.array_equal(p.binmap_view()[i].cpu().numpy().astype(np.int16), cells)
+        assert np.array_equal(p.planes_view()[i].cpu().numpy().view(np.uint32),
+                              O.integral_stack(cells, cfg.bins))
+    if cfg.scored:
+        np.testing.assert_allclose(p.scores[ends].cpu().numpy(), scores, rtol=1e-9,
+                                   atol=score_tol(weights))
