@@ -219,7 +219,7 @@ def cpu_baseline(cfg, seconds, frames=None):
         passes += 1
     px = passes * count * cfg.height * cfg.width
     return {"value": px / dt / 1e6, "unit": "Mpixel/s", "cores": threads, "kind": "port",
-            "sample": f"{passes} pass(es) over {count} of {cfg.frames} {cfg.key} frames "
+            "sample": f"{passes} pass(es) over {count} {cfg.key} frames ({cfg.frames} per step) "
                       f"(oracle/hog_oracle.c, {threads} threads, {dt:.1f} s; 1 frame on 1 thread: "
                       f"{t1 * 1e3:.0f} ms)",
             "single_thread_mpx_s": cfg.height * cfg.width / t1 / 1e6}
