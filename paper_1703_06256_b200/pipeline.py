@@ -151,7 +151,8 @@ class HogPipeline:
     def _tune_band_rows(self) -> int:
         """Time binning + carry scan + planes (+ grid) at a few band rows on this
         pipeline's own buffers and keep the fastest; the automatic choice stays
-        unless another is > 2 % faster.  Measured on B200, the best R moves
+        unless another is > 0.5 % faster (c2: R = 64 beats the automatic 128 by
+        0.9 % with the register-resident top row).  Measured on B200, the best R moves
         with the CTA-wave count of the shape (profiles/r1b_band_sweep.txt: c4
         best at 80, 8K pyramid level 1 at 40, c2/c3/level 0 at the automatic R).
         Any R gives bit-identical outputs; only the tiling changes."""
@@ -165,7 +166,7 @@ class HogPipeline:
             self.band_rows = r
             self._alloc_scratch()
             best = None
-            for it in range(3):
+            for it in range(4):
                 e0 = t.cuda.Event(enable_timing=True)
                 e1 = t.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -177,7 +178,7 @@ class HogPipeline:
                     best = ms if best is None else min(best, ms)
             times[r] = best
         pick = min(times, key=times.get)
-        if times[pick] > 0.98 * times[auto]:
+        if times[pick] > 0.995 * times[auto]:  # min of 3 timed runs each: noise < 0.5 %
             pick = auto
         self.band_rows_timings = times
         self.band_rows = pick
