@@ -182,6 +182,7 @@ class HogPipeline:
             pick = auto
         self.band_rows_timings = times
         self.band_rows = pick
+        self.scratch = []  # exact size for the pick (the candidates' largest is not kept)
         self._alloc_scratch()
         return pick
 
