@@ -471,15 +471,23 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
     p.upload(frames)
     p.run()
     torch.cuda.synchronize()
-    # parity gate: the three smallest levels of frame 0 against the oracle
-    g = O.Geometry(64, 128, 8, 1, 1, cfg.bins)
+    # parity gate: every pyramid level of frame 0 against the oracle (one
+    # level per host thread; ctypes drops the GIL)
+    from concurrent.futures import ThreadPoolExecutor
+
     lut = O.build_lut(cfg.bins)
-    for (level, factor, lw, lh) in p.levels[-3:]:
-        img = O.resize_bilinear(frames[0], lw, lh)
-        ref = O.scan_scores(O.integral_stack(O.gradient_map(img, lut), cfg.bins), g, cfg.stride,
-                            weights, bias)
+
+    def ref_level(lv):
+        level, _, lw, lh = lv
+        img = frames[0] if level == 0 else O.resize_bilinear(frames[0], lw, lh)
+        return O.run_batch(img[None], lut, cfg.bins, 8, 64, 128, cfg.stride, 1, weights, bias,
+                           threads=1, want_outputs=True)[2][0]
+
+    with ThreadPoolExecutor(max_workers=host_threads()) as pool:
+        refs = list(pool.map(ref_level, p.levels))
+    for (level, _, _, _), ref in zip(p.levels, refs):
         got = p.scores[level][0].cpu().numpy()
-        if (np.abs(got - ref) > 1e-5 * np.abs(ref) + 1e-12).any():
+        if got.shape != ref.shape or (np.abs(got - ref) > 1e-5 * np.abs(ref) + 1e-12).any():
             raise PathMismatch(f"pyramid level {level} scores differ from the oracle")
     K, W = args.steps, args.warmup
     for _ in range(W):

@@ -240,6 +240,14 @@ int hog_nms(const int32_t *boxes, const double *scores, const double *scales, in
             double iou_threshold, int32_t *keep, int32_t *keep_count, void *scratch,
             size_t scratch_bytes, hog_stream_t stream);
 
+/* detector.py:285-299 (nms) for boxes with float64 (x, y, w, h): any
+ * Detection a caller builds, e.g. non-integer coordinates.  Same order and
+ * rule as hog_nms; the IoU rounds once per double operation in Python's
+ * order (detector.py:272-282).  Scratch: hog_nms_scratch_bytes(n). */
+int hog_nms_f64(const double *boxes, const double *scores, const double *scales, int n,
+                double iou_threshold, int32_t *keep, int32_t *keep_count, void *scratch,
+                size_t scratch_bytes, hog_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

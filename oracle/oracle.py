@@ -267,10 +267,12 @@ def iou(a, b) -> float:
     return inter / (aw * ah + bw * bh - inter)
 
 
-def nms(boxes, scores, scales, iou_threshold) -> np.ndarray:
+def nms(boxes, scores, scales, iou_threshold, float_boxes=False) -> np.ndarray:
     """detector.py:285-299: kept indices, in keep order.  sorted() is stable,
-    so equal keys keep input order, as in the reference."""
-    boxes = [tuple(int(v) for v in b) for b in np.asarray(boxes)]
+    so equal keys keep input order, as in the reference.  float_boxes: box
+    coordinates stay Python floats (a caller's own Detections)."""
+    conv = float if float_boxes else int
+    boxes = [tuple(conv(v) for v in b) for b in np.asarray(boxes)]
     order = sorted(range(len(boxes)),
                    key=lambda i: (-float(scores[i]), boxes[i][1], boxes[i][0], float(scales[i])))
     kept = []

@@ -47,6 +47,7 @@ SIGNATURES = {
                         _SZ, _P]),
     "hog_nms_scratch_bytes": (_SZ, [_I]),
     "hog_nms": (_I, [_P, _P, _P, _I, _D, _P, _P, _P, _SZ, _P]),
+    "hog_nms_f64": (_I, [_P, _P, _P, _I, _D, _P, _P, _P, _SZ, _P]),
 }
 
 

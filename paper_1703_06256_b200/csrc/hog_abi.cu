@@ -91,7 +91,7 @@ TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int ce
     // store-bound, and staging adds shared-memory traffic and 9% instructions
     // (profiles/r1_tma_store_ab.md).  Pure stores do reach 7.2 TB/s this way
     // (tools/probe_tma_store.cu) against 5.5 TB/s for st.global.
-    tma = tma && env_int("HOGB200_TMA", 0) != 0;
+    tma = HOGB200_VARIANTS && tma && env_int("HOGB200_TMA", 0) != 0;
     // top row in registers when a band's strips fit the 6-warp variant (c2: 6
     // strips; measured 1.153 -> 1.136 ms); wider small-bin frames keep 8 warps
     g.PREG = (K2_PTOP_REG && 2 * g.NW * g.VC <= 32 && !tma && g.ns <= 6 &&
@@ -113,8 +113,10 @@ TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int ce
     } else {
         while (R > 16 && (int64_t)n * (h / R + 1) * g.NWARP < 148 * 32) R /= 2;
     }
-    if (fused && R % stride != 0) R = (int)round_up(R, stride);
-    if (R > 240) R = 240;  // u8 column counts; packed strip-local sums stay < 2^16
+    // u8 column counts and packed strip-local sums (< 2^16) bound R at 240;
+    // clamp first, then keep R a multiple of the lattice step (fused grid)
+    if (R > 240) R = 240;
+    if (fused && R % stride != 0) R = R / stride * stride > 0 ? R / stride * stride : stride;
     g.R = R;
     // k_grad_bin runs R1 = R / S1 row sub-bands per warp, so its grid is several
     // waves deep (one R-row band per warp left a 1.08-wave tail on c2)
@@ -309,8 +311,9 @@ static int pipeline_impl(const uint8_t *img, int n, int c, int h, int w, int64_t
                     "hog_integral + hog_cell_grid", MAX_FUSED_BINS, bins);
     int kr = 0;
     if (grid) {
-        if (stride <= 0 || stride % 4 != 0 || cell % stride != 0 || cell / stride > 2 || cell % 4 != 0)
-            return fail(HOG_EINVAL, "fused grid needs stride %% 4 == 0, cell %% stride == 0, "
+        if (stride <= 0 || stride % 4 != 0 || cell % stride != 0 || cell / stride > 2 || cell % 4 != 0 ||
+            stride > 240)
+            return fail(HOG_EINVAL, "fused grid needs stride %% 4 == 0, stride <= 240, cell %% stride == 0, "
                         "cell/stride <= 2 (stride %d, cell %d)", stride, cell);
         if (ncx < 1 || ncy < 1 || (int64_t)(ncx - 1) * stride + cell > w ||
             (int64_t)(ncy - 1) * stride + cell > h)
@@ -322,7 +325,8 @@ static int pipeline_impl(const uint8_t *img, int n, int c, int h, int w, int64_t
     PlaneOut po = make_po(pl, pp, pns, pfs, w);
     // the fused-binning variant (opt-in, below) keeps per-thread plane stores
     const char *fenv = getenv("HOGB200_FUSED");
-    const bool want_fused = (stages & HOG_STAGE_ALL) == HOG_STAGE_ALL && po.vec && fenv && fenv[0] == '1';
+    const bool want_fused = HOGB200_VARIANTS && (stages & HOG_STAGE_ALL) == HOG_STAGE_ALL && po.vec &&
+                            fenv && fenv[0] == '1';
     TileGeom g = make_geom(n, h, w, bins, kr > 0, stride, cell, v8_ok(po, bm, bp, bfs),
                            po.vec != 0 && !want_fused);
     g.ht = halo_top ? 1 : 0;
@@ -551,24 +555,43 @@ int hog_detect(const double *scores, int n, int noy, int nox, double threshold, 
 
 size_t hog_nms_scratch_bytes(int n) { return n < 1 ? 0 : nms_scratch_bytes(n); }
 
-int hog_nms(const int32_t *boxes, const double *scores, const double *scales, int n,
-            double iou_threshold, int32_t *keep, int32_t *keep_count, void *scratch, size_t sbytes,
-            hog_stream_t stream) {
+}  // extern "C"
+
+template <typename B, typename L>
+static int nms_impl(const B *boxes, const double *scores, const double *scales, int n,
+                    double iou_threshold, int32_t *keep, int32_t *keep_count, void *scratch,
+                    size_t sbytes, hog_stream_t stream, L launch, const char *what) {
     g_err.clear();
     if (!(iou_threshold >= 0.0 && iou_threshold <= 1.0))
         return fail(HOG_EINVAL, "iou_threshold must be in [0, 1], got %g", iou_threshold);
     if (n < 0 || !keep_count) return fail(HOG_EINVAL, "bad arguments");
     if (n == 0) {
         cudaMemsetAsync(keep_count, 0, sizeof(int32_t), (cudaStream_t)stream);
-        return check_launch("hog_nms");
+        return check_launch(what);
     }
     if (!boxes || !scores || !scales || !keep || !scratch) return fail(HOG_EINVAL, "null buffer");
     if (sbytes < nms_scratch_bytes(n))
         return fail(HOG_EINVAL, "scratch too small: need %zu bytes", nms_scratch_bytes(n));
-    if (launch_nms(boxes, scores, scales, n, iou_threshold, keep, keep_count, scratch, sbytes,
-                   (cudaStream_t)stream) != 0)
-        return fail(HOG_ECUDA, "hog_nms: sort failed");
-    return check_launch("hog_nms");
+    if (launch(boxes, scores, scales, n, iou_threshold, keep, keep_count, scratch, sbytes,
+               (cudaStream_t)stream) != 0)
+        return fail(HOG_ECUDA, "%s: sort failed", what);
+    return check_launch(what);
+}
+
+extern "C" {
+
+int hog_nms_f64(const double *boxes, const double *scores, const double *scales, int n,
+                double iou_threshold, int32_t *keep, int32_t *keep_count, void *scratch,
+                size_t sbytes, hog_stream_t stream) {
+    return nms_impl(boxes, scores, scales, n, iou_threshold, keep, keep_count, scratch, sbytes,
+                    stream, launch_nms_f64, "hog_nms_f64");
+}
+
+int hog_nms(const int32_t *boxes, const double *scores, const double *scales, int n,
+            double iou_threshold, int32_t *keep, int32_t *keep_count, void *scratch, size_t sbytes,
+            hog_stream_t stream) {
+    return nms_impl(boxes, scores, scales, n, iou_threshold, keep, keep_count, scratch, sbytes,
+                    stream, launch_nms, "hog_nms");
 }
 
 }  // extern "C"

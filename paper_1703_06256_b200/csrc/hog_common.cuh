@@ -14,6 +14,14 @@
 
 #include "../../include/hogb200.h"
 
+// Measured-and-lost variants (TMA bulk-store plane path, binning fused into
+// the plane kernel with decoupled look-back, the first lattice score kernel)
+// are compiled only into experiment builds (tools/build_variant.sh passes
+// -DHOGB200_VARIANTS=1); the product library holds the measured-best paths.
+#ifndef HOGB200_VARIANTS
+#define HOGB200_VARIANTS 0
+#endif
+
 namespace hogb200 {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -349,6 +357,8 @@ size_t det_scratch_bytes(int n, int64_t m);
 size_t nms_scratch_bytes(int n);
 int launch_nms(const int32_t *boxes, const double *scores, const double *scales, int n, double thr,
                int32_t *keep, int32_t *keep_count, void *scratch, size_t sbytes, cudaStream_t st);
+int launch_nms_f64(const double *boxes, const double *scores, const double *scales, int n, double thr,
+                   int32_t *keep, int32_t *keep_count, void *scratch, size_t sbytes, cudaStream_t st);
 void launch_detect_abi(const double *scores, int n, int noy, int nox, double thr, const int32_t *oxs,
                        const int32_t *oys, double scale, int ww, int wh, int clamp_w, int clamp_h,
                        int cap, int32_t *boxes, double *out_scores, int64_t *out_window,

@@ -143,19 +143,28 @@ __global__ void k_det_scatter(const double *__restrict__ scores, int64_t m, int 
 // ---------------------------------------------------------------------------
 // NMS
 
+// Boxes are (x, y, w, h) as int32 (what hog_detect emits) or as float64
+// (any Detection a caller builds); the IoU follows detector.py:272-282 in
+// the box type's arithmetic: integer sums and differences, then one rounding
+// per double operation in Python's order (no FMA contraction).
+template <typename B>
 struct NmsLess {  // detector.py:292: key (-score, y, x, scale)
-    const int32_t *boxes;
+    const B *boxes;
     const double *scores, *scales;
     __device__ bool operator()(int a, int b) const {
         const double sa = scores[a], sb = scores[b];
         if (sa != sb) return sa > sb;
-        const int ya = boxes[4 * a + 1], yb = boxes[4 * b + 1];
+        const B ya = boxes[4 * a + 1], yb = boxes[4 * b + 1];
         if (ya != yb) return ya < yb;
-        const int xa = boxes[4 * a], xb = boxes[4 * b];
+        const B xa = boxes[4 * a], xb = boxes[4 * b];
         if (xa != xb) return xa < xb;
         return scales[a] < scales[b];
     }
 };
+
+template <typename B> struct Box4;
+template <> struct Box4<int32_t> { using T = int4; };
+template <> struct Box4<double> { using T = double4; };
 
 __device__ __forceinline__ double box_iou(int4 a, int4 b) {  // detector.py:272-282
     const double ix = fmax(0.0, (double)(min(a.x + a.z, b.x + b.z) - max(a.x, b.x)));
@@ -166,6 +175,15 @@ __device__ __forceinline__ double box_iou(int4 a, int4 b) {  // detector.py:272-
     return inter / uni;
 }
 
+__device__ __forceinline__ double box_iou(double4 a, double4 b) {  // detector.py:272-282
+    const double ix = fmax(0.0, __dsub_rn(fmin(__dadd_rn(a.x, a.z), __dadd_rn(b.x, b.z)), fmax(a.x, b.x)));
+    const double iy = fmax(0.0, __dsub_rn(fmin(__dadd_rn(a.y, a.w), __dadd_rn(b.y, b.w)), fmax(a.y, b.y)));
+    const double inter = __dmul_rn(ix, iy);
+    if (inter <= 0.0) return 0.0;
+    const double uni = __dsub_rn(__dadd_rn(__dmul_rn(a.z, a.w), __dmul_rn(b.z, b.w)), inter);
+    return __ddiv_rn(inter, uni);
+}
+
 constexpr int NMS_B = 1024;
 
 __global__ void k_iota(int32_t *v, int n) {
@@ -174,22 +192,25 @@ __global__ void k_iota(int32_t *v, int n) {
 }
 
 // one CTA of NMS_B threads; mask scratch: NMS_B x NMS_B/32 words
+template <typename B>
 __global__ void __launch_bounds__(NMS_B)
-k_nms_greedy(const int32_t *__restrict__ boxes, const int32_t *__restrict__ order, int n, double thr,
-             uint32_t *__restrict__ mask, int4 *__restrict__ kept_box, int32_t *__restrict__ keep,
-             int32_t *__restrict__ keep_count) {
-    __shared__ int4 blk[NMS_B];
-    __shared__ unsigned char sup[NMS_B];
+k_nms_greedy(const B *__restrict__ boxes, const int32_t *__restrict__ order, int n, double thr,
+             uint32_t *__restrict__ mask, typename Box4<B>::T *__restrict__ kept_box,
+             int32_t *__restrict__ keep, int32_t *__restrict__ keep_count) {
+    using T = typename Box4<B>::T;
+    extern __shared__ __align__(16) unsigned char nms_smem[];
+    T *blk = reinterpret_cast<T *>(nms_smem);                         // [NMS_B]
+    int *blk_keep_idx = reinterpret_cast<int *>(blk + NMS_B);         // [NMS_B]
+    unsigned char *sup = reinterpret_cast<unsigned char *>(blk_keep_idx + NMS_B);  // [NMS_B]
     __shared__ int kept_n, blk_kept;
-    __shared__ int blk_keep_idx[NMS_B];
     const int tid = threadIdx.x, lane = tid & 31;
     if (tid == 0) kept_n = 0;
     __syncthreads();
     for (int base = 0; base < n; base += NMS_B) {
         const int i = base + tid;
         const bool valid = i < n;
-        int4 bx = make_int4(0, 0, 0, 0);
-        if (valid) bx = reinterpret_cast<const int4 *>(boxes)[order[i]];
+        T bx{};
+        if (valid) bx = reinterpret_cast<const T *>(boxes)[order[i]];
         blk[tid] = bx;
         // (1) against every box kept in earlier blocks
         bool s = !valid;
@@ -240,19 +261,27 @@ k_nms_greedy(const int32_t *__restrict__ boxes, const int32_t *__restrict__ orde
     if (tid == 0) *keep_count = kept_n;
 }
 
-size_t nms_scratch_bytes(int n) {
+template <typename B>
+static size_t nms_scratch_t(int n) {
     size_t sort_bytes = 0;
-    NmsLess less{nullptr, nullptr, nullptr};
+    NmsLess<B> less{nullptr, nullptr, nullptr};
     cub::DeviceMergeSort::StableSortKeys(nullptr, sort_bytes, (int32_t *)nullptr, n, less);
     auto r = [](size_t b) { return (b + 255) / 256 * 256; };
-    return r(sort_bytes) + r(sizeof(int32_t) * (size_t)n) + r(sizeof(int4) * (size_t)n) +
+    return r(sort_bytes) + r(sizeof(int32_t) * (size_t)n) + r(sizeof(typename Box4<B>::T) * (size_t)n) +
            r(sizeof(uint32_t) * (size_t)NMS_B * (NMS_B / 32));
 }
 
-int launch_nms(const int32_t *boxes, const double *scores, const double *scales, int n, double thr,
-               int32_t *keep, int32_t *keep_count, void *scratch, size_t sbytes, cudaStream_t st) {
+size_t nms_scratch_bytes(int n) {
+    const size_t a = nms_scratch_t<int32_t>(n), b = nms_scratch_t<double>(n);
+    return a > b ? a : b;
+}
+
+template <typename B>
+static int launch_nms_t(const B *boxes, const double *scores, const double *scales, int n, double thr,
+                        int32_t *keep, int32_t *keep_count, void *scratch, cudaStream_t st) {
+    using T = typename Box4<B>::T;
     size_t sort_bytes = 0;
-    NmsLess less{boxes, scores, scales};
+    NmsLess<B> less{boxes, scores, scales};
     cub::DeviceMergeSort::StableSortKeys(nullptr, sort_bytes, (int32_t *)nullptr, n, less);
     auto r = [](size_t b) { return (b + 255) / 256 * 256; };
     char *p = (char *)scratch;
@@ -260,14 +289,30 @@ int launch_nms(const int32_t *boxes, const double *scores, const double *scales,
     p += r(sort_bytes);
     int32_t *order = (int32_t *)p;
     p += r(sizeof(int32_t) * (size_t)n);
-    int4 *kept_box = (int4 *)p;
-    p += r(sizeof(int4) * (size_t)n);
+    T *kept_box = (T *)p;
+    p += r(sizeof(T) * (size_t)n);
     uint32_t *mask = (uint32_t *)p;
     k_iota<<<blocks_for(n, 256), 256, 0, st>>>(order, n);
     if (cub::DeviceMergeSort::StableSortKeys(tmp, sort_bytes, order, n, less, st) != cudaSuccess)
         return -1;
-    k_nms_greedy<<<1, NMS_B, 0, st>>>(boxes, order, n, thr, mask, kept_box, keep, keep_count);
+    const size_t smem = (sizeof(T) + sizeof(int) + 1) * NMS_B;
+    static size_t configured[HOG_MAX_DEVICES] = {};
+    if (smem_optin_needed(configured, smem))
+        cudaFuncSetAttribute(k_nms_greedy<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_nms_greedy<B><<<1, NMS_B, smem, st>>>(boxes, order, n, thr, mask, kept_box, keep, keep_count);
     return 0;
+}
+
+int launch_nms(const int32_t *boxes, const double *scores, const double *scales, int n, double thr,
+               int32_t *keep, int32_t *keep_count, void *scratch, size_t sbytes, cudaStream_t st) {
+    (void)sbytes;
+    return launch_nms_t<int32_t>(boxes, scores, scales, n, thr, keep, keep_count, scratch, st);
+}
+
+int launch_nms_f64(const double *boxes, const double *scores, const double *scales, int n, double thr,
+                   int32_t *keep, int32_t *keep_count, void *scratch, size_t sbytes, cudaStream_t st) {
+    (void)sbytes;
+    return launch_nms_t<double>(boxes, scores, scales, n, thr, keep, keep_count, scratch, st);
 }
 
 size_t det_scratch_bytes(int n, int64_t m) {

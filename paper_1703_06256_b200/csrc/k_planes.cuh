@@ -733,23 +733,25 @@ template <int NW, int KR>
 void launch_planes_kr(int ch, const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
                       const GridOut &go, const TileGeom &g, const Scratch &sc, const FusedIn &fi,
                       cudaStream_t st) {
-    if (ch == 1) {  // fused, grayscale
-        if constexpr (NW <= 5) {
-            if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 1>(bm, bp, bfs, po, go, g, sc, fi, st);
+    if constexpr (HOGB200_VARIANTS) {  // experiment builds only (measured slower)
+        if (ch == 1) {  // fused, grayscale
+            if constexpr (NW <= 5) {
+                if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 1>(bm, bp, bfs, po, go, g, sc, fi, st);
+            }
+            return launch_planes_vc<NW, KR, 4, true, 1>(bm, bp, bfs, po, go, g, sc, fi, st);
         }
-        return launch_planes_vc<NW, KR, 4, true, 1>(bm, bp, bfs, po, go, g, sc, fi, st);
-    }
-    if (ch == 3) {  // fused, RGB
-        if constexpr (NW <= 5) {
-            if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 3>(bm, bp, bfs, po, go, g, sc, fi, st);
+        if (ch == 3) {  // fused, RGB
+            if constexpr (NW <= 5) {
+                if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 3>(bm, bp, bfs, po, go, g, sc, fi, st);
+            }
+            return launch_planes_vc<NW, KR, 4, true, 3>(bm, bp, bfs, po, go, g, sc, fi, st);
         }
-        return launch_planes_vc<NW, KR, 4, true, 3>(bm, bp, bfs, po, go, g, sc, fi, st);
-    }
-    if (g.TMA) {  // plane rows through shared memory and TMA bulk stores (requires po.vec)
-        if constexpr (NW <= 5) {
-            if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 0, true>(bm, bp, bfs, po, go, g, sc, fi, st);
+        if (g.TMA) {  // plane rows through shared memory and TMA bulk stores (requires po.vec)
+            if constexpr (NW <= 5) {
+                if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 0, true>(bm, bp, bfs, po, go, g, sc, fi, st);
+            }
+            return launch_planes_vc<NW, KR, 4, true, 0, true>(bm, bp, bfs, po, go, g, sc, fi, st);
         }
-        return launch_planes_vc<NW, KR, 4, true, 0, true>(bm, bp, bfs, po, go, g, sc, fi, st);
     }
     if constexpr (NW <= 5) {
         if (g.VC == 8) return launch_planes_vc<NW, KR, 8, true, 0>(bm, bp, bfs, po, go, g, sc, fi, st);

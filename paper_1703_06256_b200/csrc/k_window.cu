@@ -340,7 +340,7 @@ void launch_window_features(const int32_t *grid, int n, int ncy, int ncx, int bi
 void launch_scores_lattice(const int32_t *grid, const double *den, int n, int ncy, int ncx,
                            int bins, int noy, int nox, int cells_y, int k, const double *wts,
                            double bias, double *scores, cudaStream_t st) {
-    if (den == nullptr && getenv("HOGB200_SCORES_V1") == nullptr)  // k_scores.cu (integer grid)
+    if (den == nullptr && !(HOGB200_VARIANTS && getenv("HOGB200_SCORES_V1")))  // k_scores.cu (integer grid)
         return launch_scores_rows(grid, n, ncy, ncx, bins, noy, nox, cells_y, k, wts, bias, scores, st);
     const int span = SC_COLS + 7 * k;
     const size_t smem =

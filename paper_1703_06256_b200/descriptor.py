@@ -133,10 +133,16 @@ def window_features_device(grid, g: DescriptorGeometry, row_idx, col_idx, weight
     ri = t.as_tensor(np.ascontiguousarray(row_idx, dtype=np.int32), device=dev)
     ci = t.as_tensor(np.ascontiguousarray(col_idx, dtype=np.int32), device=dev)
     noy, nox = ri.shape[0], ci.shape[0]
-    Dn = descriptor_length(g)
+    # the descriptor carries the GRID's bins (the stack's), as _assemble_blocks
+    # does (descriptor.py:107-124); the kernel strides by them too
+    Dn = g.blocks_x * g.blocks_y * g.block * g.block * bins
     scores = desc = wt = None
     if want_scores:
-        wt = t.as_tensor(np.ascontiguousarray(weights, dtype=np.float64), device=dev)
+        wt = np.ascontiguousarray(weights, dtype=np.float64)
+        if wt.ndim != 1 or len(wt) != Dn:  # np.dot(w, desc) raises here (detector.py:148-150)
+            raise ValueError(f"shapes ({len(wt)},) and ({Dn},) not aligned: weights length "
+                             f"{len(wt)} != descriptor length {Dn} ({bins} bins)")
+        wt = t.as_tensor(wt, device=dev)
         scores = t.empty((n, noy, nox), dtype=t.float64, device=dev)
     if want_desc:
         desc = t.empty((n, noy, nox, Dn), dtype=t.float64, device=dev)
@@ -198,8 +204,15 @@ class CellHistogramCache:
     resident for the window stage.
     """
 
+    # descriptors are materialised on the device a block of window rows at a
+    # time (about this many values per block) and kept on the host, so a
+    # reference-style per-window loop (detector.py:140-154) costs one launch
+    # and one copy per block, not per window
+    BLOCK_VALUES = 1 << 22
+
     def __init__(self, stack: IntegralStack, g: DescriptorGeometry, origin_xs, origin_ys):
         self.geometry = g
+        self.bins = stack.bins  # the grid's bins are the stack's (descriptor.py:176-185)
         cell_xs, cell_ys, self.col_idx, self.row_idx = cell_lattice(origin_xs, origin_ys, g)
         self.cell_xs, self.cell_ys = cell_xs, cell_ys
         if len(cell_xs) and len(cell_ys):
@@ -207,12 +220,13 @@ class CellHistogramCache:
         else:
             self.device_grid = None
         self._grid = None
+        self._block = None  # (first window row, last + 1, descriptors (rows, nox, D))
 
     @property
     def grid(self) -> np.ndarray:
         if self._grid is None:
             if self.device_grid is None:
-                gr = np.zeros((len(self.cell_ys), len(self.cell_xs), self.geometry.bins), np.int64)
+                gr = np.zeros((len(self.cell_ys), len(self.cell_xs), self.bins), np.int64)
             else:
                 gr = self.device_grid[0].cpu().numpy().astype(np.int64)
             gr.setflags(write=False)
@@ -222,11 +236,22 @@ class CellHistogramCache:
     def window_cells(self, origin_ix: int, origin_iy: int) -> np.ndarray:
         return self.grid[np.ix_(self.row_idx[origin_iy], self.col_idx[origin_ix])]
 
+    def rows_per_block(self) -> int:
+        g = self.geometry
+        per_row = max(1, len(self.col_idx) * g.blocks_x * g.blocks_y * g.block * g.block * self.bins)
+        return max(1, self.BLOCK_VALUES // per_row)
+
     def descriptor(self, origin_ix: int, origin_iy: int) -> np.ndarray:
-        _, desc = window_features_device(self.device_grid, self.geometry,
-                                         self.row_idx[origin_iy][None],
-                                         self.col_idx[origin_ix][None], want_desc=True)
-        return _as_reference_dtype(desc[0, 0, 0].cpu().numpy(), self.geometry)
+        """descriptor.py:194-195.  The window row's block of descriptors is
+        assembled on the device on first use and served from the host copy."""
+        iy = range(len(self.row_idx))[origin_iy]  # IndexError / negative index as numpy
+        ix = range(len(self.col_idx))[origin_ix]
+        blk = self._block
+        if blk is None or not blk[0] <= iy < blk[1]:
+            r0 = iy - iy % self.rows_per_block()
+            r1 = min(len(self.row_idx), r0 + self.rows_per_block())
+            blk = self._block = (r0, r1, self.descriptors(slice(r0, r1)))
+        return blk[2][iy - blk[0], ix].copy()
 
     def descriptors(self, iy_range=None):
         """All descriptors of window rows iy_range as (rows, nox, D), one launch."""
@@ -253,8 +278,7 @@ def scan_descriptors(stack: IntegralStack, g: DescriptorGeometry, stride: int):
             f"window {g.window_w}x{g.window_h} exceeds {stack.width}x{stack.height}")
     oxs, oys = window_origins(stack.width, stack.height, g, stride)
     cache = CellHistogramCache(stack, g, oxs, oys)
-    per_row = max(1, len(oxs) * descriptor_length(g))
-    chunk = max(1, (1 << 22) // per_row)
+    chunk = cache.rows_per_block()
     for r0 in range(0, len(oys), chunk):
         block = cache.descriptors(slice(r0, min(r0 + chunk, len(oys))))
         for j in range(block.shape[0]):

@@ -55,7 +55,8 @@ def compact(scores, oxs, oys, threshold: float, scale: float, ww: int, wh: int,
 
 def nms_indices(boxes, scores, scales, iou_threshold: float, stream=None) -> np.ndarray:
     """detector.py:285-299 on the device: kept indices into the (N, 4) int32
-    boxes / (N,) float64 scores / scales device tensors, in keep order."""
+    or float64 boxes / (N,) float64 scores / scales device tensors, in keep
+    order (int32 boxes: hog_nms; float64 boxes: hog_nms_f64)."""
     t = D.require_cuda()
     n = int(boxes.shape[0])
     if n == 0:
@@ -67,7 +68,10 @@ def nms_indices(boxes, scores, scales, iou_threshold: float, stream=None) -> np.
     keep = t.empty(n, dtype=t.int32, device=dev)
     kc = t.zeros(1, dtype=t.int32, device=dev)
     boxes, scores, scales = boxes.contiguous(), scores.contiguous(), scales.contiguous()
-    _native.call("hog_nms", D.ptr(boxes), D.ptr(scores), D.ptr(scales), n, float(iou_threshold),
+    fn = "hog_nms_f64" if boxes.dtype == t.float64 else "hog_nms"
+    if fn == "hog_nms" and boxes.dtype != t.int32:
+        raise TypeError(f"boxes must be int32 or float64, got {boxes.dtype}")
+    _native.call(fn, D.ptr(boxes), D.ptr(scores), D.ptr(scales), n, float(iou_threshold),
                  D.ptr(keep), D.ptr(kc), D.ptr(scratch), sb, D.stream_handle(stream))
     k = int(kc.item())
     return keep[:k].cpu().numpy().astype(np.int64)

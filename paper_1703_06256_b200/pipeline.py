@@ -15,6 +15,7 @@ give each rank its own pipeline over its own frame shard, with no collective.
 from __future__ import annotations
 
 import ctypes
+import functools
 
 import numpy as np
 
@@ -24,9 +25,21 @@ from .descriptor import (DescriptorGeometry, cell_lattice, descriptor_length, ep
 from .gradient import build_lut
 
 
+def on_device(fn):
+    """Run a pipeline method with the pipeline's device current: the C ABI
+    launches on the CUDA runtime's current device, and per-device state
+    (shared-memory opt-in, streams) follows it.  One host thread can then
+    drive pipelines on several GPUs."""
+    @functools.wraps(fn)
+    def wrap(self, *args, **kwargs):
+        with D.torch().cuda.device(self.device):
+            return fn(self, *args, **kwargs)
+    return wrap
+
+
 def regular_lattice(cell_xs, cell_ys, stride: int, cell: int, bins: int) -> bool:
     """True when hog_pipeline can emit the grid from the plane kernel."""
-    if stride % 4 or cell % stride or cell // stride > 2 or cell % 4 or bins > 18:
+    if stride % 4 or stride > 240 or cell % stride or cell // stride > 2 or cell % 4 or bins > 18:
         return False
     for cs in (cell_xs, cell_ys):
         if len(cs) == 0 or not np.array_equal(cs, np.arange(0, cs[-1] + 1, stride)):
@@ -148,6 +161,7 @@ class HogPipeline:
                                                     self.stride if self.fused else 0,
                                                     self.cell if self.fused else 0))
 
+    @on_device
     def _tune_band_rows(self) -> int:
         """Time binning + carry scan + planes (+ grid) at a few band rows on this
         pipeline's own buffers and keep the fastest; the automatic choice stays
@@ -187,6 +201,7 @@ class HogPipeline:
         return pick
 
     # -- data movement ------------------------------------------------------
+    @on_device
     def upload(self, frames: np.ndarray, stream=None):
         t = D.torch()
         src = t.from_numpy(np.ascontiguousarray(frames))
@@ -222,6 +237,7 @@ class HogPipeline:
                      D.ptr(scr), sb, stages | (_native.STAGE_GRID_U8 if self.grid_u8 else 0), evs,
                      D.stream_handle(stream))
 
+    @on_device
     def run(self, stream=None, plane_events=None, frames_ptr=None, scores_ptr=None,
             pipelined: bool = False):
         """Enqueue the whole batch; results are ready in `stream` order (default:
@@ -287,6 +303,7 @@ class HogPipeline:
             return
         self._post(main, scores_ptr)
 
+    @on_device
     def join(self, stream=None):
         """Make `stream` wait for the scores of the last pipelined run."""
         if self._post_done is not None:
@@ -295,6 +312,7 @@ class HogPipeline:
                 self._post_done)
             self._post_done = None
 
+    @on_device
     def run_staged(self, events, stream=None):
         """Diagnostic: the whole batch as one chunk with 4 recorded events
         bracketing binning, carry scan and planes (+ grid)."""
@@ -303,9 +321,7 @@ class HogPipeline:
         self.join(main)
         saved = self.ranges, self.scratch
         if self.chunks > 1:  # one chunk needs the whole-batch scratch
-            sb = int(_native.load().hog_scratch_bytes(self.n, self.h, self.w, self.bins,
-                                                      self.stride if self.fused else 0,
-                                                      self.cell if self.fused else 0))
+            sb = self._scratch_bytes(0, self.n)  # sized at this pipeline's band rows
             self.ranges = [(0, self.n)]
             self.scratch = [(t.empty(max(sb, 256), dtype=t.uint8, device=self.device), sb)]
         try:
@@ -352,6 +368,7 @@ class HogPipeline:
                          eps_term(g.normalization), D.ptr(self.w_dev), self.bias,
                          sp, None, s)
 
+    @on_device
     def detections(self, threshold: float, iou_threshold: float | None = None, scale: float = 1.0):
         """Per-frame detection lists of the last run (needs weights): windows with
         score > threshold in row-major order (detector.py:145-153, 194-199),
@@ -481,6 +498,7 @@ class PyramidPipeline:
         self.streams = max(1, min(int(streams), len(self.levels)))
         self._side = [t.cuda.Stream(device=self.device) for _ in range(self.streams - 1)]
 
+    @on_device
     def upload(self, frames: np.ndarray):
         t = D.torch()
         src = t.from_numpy(np.ascontiguousarray(frames))
@@ -489,6 +507,7 @@ class PyramidPipeline:
         else:
             self.src.data[..., : self.w].copy_(src, non_blocking=True)
 
+    @on_device
     def run(self, stream=None, plane_events=None, chunk_ready=None, level_done=None):
         """plane_events: optional list; (start, end, algorithmic bytes) of every
         plane-kernel launch is appended (events recorded on the launch stream).
@@ -570,6 +589,7 @@ class PyramidPipeline:
                         for (lv, _, _, _), p in zip(self.levels, self.pipes))
         return per_chunk * ((self.n + self.chunk - 1) // self.chunk)
 
+    @on_device
     def detections(self, frame: int, threshold: float, iou_threshold: float | None = None,
                    window=(64, 128)):
         """One frame's boxes as pyramid_scan returns them (detector.py:252-268),

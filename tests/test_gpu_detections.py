@@ -150,3 +150,32 @@ def test_nms_api_greedy_definition():
         assert [k.score for k in kept] == sorted([k.score for k in kept], reverse=True)
         ref = O.nms([d.box for d in dets], [d.score for d in dets], [d.scale for d in dets], thr)
         assert [id(k) for k in kept] == [id(dets[i]) for i in ref]
+
+
+def test_random_nms_float_boxes_vs_oracle():
+    """Non-integer boxes (a caller's own Detections) take hog_nms_f64: same
+    keep list as the reference's Python-float IoU, including y/x ties."""
+    rng = np.random.default_rng(7)
+    k = 2500
+    boxes = np.stack([rng.integers(0, 300, k) / 3.0, rng.integers(0, 200, k) * 0.1,
+                      rng.integers(12, 600, k) / 3.0, rng.integers(40, 2000, k) * 0.1], 1)
+    scores = np.round(rng.normal(0, 1, k), 1)  # many score ties -> (y, x, scale) order
+    scales = rng.choice([1.0, 1.2, 1.44], k)
+    for t in (0.0, 0.3, 0.5, 1.0):
+        keep = DT.nms_indices(dev(boxes, np.float64), dev(scores, np.float64),
+                              dev(scales, np.float64), t)
+        assert np.array_equal(keep, O.nms(boxes, scores, scales, t, float_boxes=True))
+
+
+def test_nms_api_float_detections():
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        dets = [H.Detection(float(rng.integers(0, 80)) / 4, float(rng.integers(0, 80)) / 4,
+                            float(rng.integers(8, 80)) / 4, float(rng.integers(8, 80)) / 4,
+                            float(np.round(rng.normal(), 1)), float(rng.choice([1.0, 1.2])))
+                for _ in range(int(rng.integers(1, 40)))]
+        thr = float(rng.uniform(0, 1))
+        kept = H.nms(dets, thr)
+        ref = O.nms([d.box for d in dets], [d.score for d in dets], [d.scale for d in dets], thr,
+                    float_boxes=True)
+        assert [id(k) for k in kept] == [id(dets[i]) for i in ref]
