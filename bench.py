@@ -7,8 +7,12 @@ A step is one pass of the hot path (LUT binning -> N_b int32 integral planes
 -> cell-histogram grid [-> per-cell L2 / window scores]) over one batch of a
 BASELINE configuration (default c2 = BASELINE.json configs[1]: 512 blurred
 640x480 frames, N_b=8, 64x128 windows at stride 4).  Frames are independent:
-under torchrun each rank runs its own batch of distinct frames (weak scaling,
-no collective on the data path); timings are max over ranks.
+under torchrun the config's batch is split into contiguous frame shards, one
+per rank (strong scaling, BASELINE "sharded across 1/2/4/8 GPUs"; no
+collective on the data path), and every rank's results land, in frame
+order, in one host buffer shared by the node's ranks (the e2e leg's
+gather); timings are max over ranks.  --scaling weak gives every rank a
+whole batch of its own instead.
 
 --impl reference times the reference algorithm's CPU implementation (the
 oracle port in oracle/, all host threads) on a bounded sample of the same
@@ -43,7 +47,22 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--frames", type=int, default=0, help="override frames per GPU (debug)")
+    ap.add_argument("--frames", type=int, default=0,
+                    help="override the batch size (strong: frames split over the ranks; "
+                         "weak: frames per rank)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's batch split over the ranks (default); "
+                         "weak: every rank runs a whole batch of distinct frames")
+    ap.add_argument("--dump-result", default="",
+                    help="rank 0 saves the gathered e2e result (whole batch, frame order) "
+                         "to this .npy path")
+    ap.add_argument("--split-frame", action="store_true",
+                    help="one frame of the config (c5: one 8K frame) cut into row slabs, one "
+                         "per rank, with the column-carry all_gather (SURVEY 8f-2); reports "
+                         "per-frame latency")
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="diagnostic: run only rank 0's shard of a W-way strong split "
+                         "(the per-GPU regime of a W-GPU run, measured on one GPU)")
     ap.add_argument("--chunks", type=int, default=0, help="override binning/plane overlap chunks")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -72,6 +91,26 @@ def workload_name(cfg) -> str:
     norm = f", per-cell {cfg.normalization}" if cfg.normalization != "none" else ""
     return (f"{cfg.key}: {cfg.frames}x {cfg.channels}x{cfg.height}x{cfg.width} u8 ({kind}{extra}), "
             f"N_b={cfg.bins}, cell 8, 64x128 windows stride {cfg.stride}{norm}{tail}")
+
+
+def bench_config(cfg, nf_global: int, world: int, scaling: str, per_rank: int) -> dict:
+    """The workload description both arms print (identical keys and values:
+    the driver compares the arms' configs)."""
+    H, W = cfg.height, cfg.width
+    return {"workload": workload_name(cfg), "global_frames": nf_global,
+            "frames_per_gpu": per_rank, "scaling": scaling,
+            "parallelism": (f"{scaling} frame split over {world} GPU(s), contiguous shards, "
+                            "no collective on the data path, results gathered in one host buffer"),
+            "l2": f"inputs larger than L2 ({nf_global * cfg.channels * H * W / 1e6:.0f} MB of frames "
+                  f"per step in, > 4 B/px of planes out, vs 126 MB L2)"}
+
+
+def shard_frames(nf_global: int, rank: int, world: int, scaling: str) -> range:
+    from paper_1703_06256_b200 import sharding
+
+    if scaling == "weak":
+        return sharding.shard(rank, world, nf_global // world)
+    return sharding.split(nf_global, rank, world)
 
 
 def measured_peak():
@@ -201,6 +240,93 @@ def cpu_sample_size(cfg, frames1, threads, seconds):
     return max(threads, min(cfg.frames, int(seconds * threads / max(t1, 1e-3)))), t1
 
 
+def host_info() -> dict:
+    """CPU model, numpy and BLAS of the host the CPU legs ran on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        b = np.show_config(mode="dicts")["Build Dependencies"]["blas"]
+        blas = f"{b.get('name')} {b.get('version')}"
+    except Exception:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "affinity_cores": host_threads(),
+            "numpy": np.__version__, "blas": blas}
+
+
+def _ref_frame(args):
+    """One frame through the vendored reference (fasthog, baseline/_ref) by
+    its public API, the way SURVEY §8d maps the config: gradient_map ->
+    build_integral_stack -> scan (threshold -inf) | scan_descriptors drained."""
+    frame, key, bins, stride, norm, scored, w, b = args
+    import fasthog as F
+
+    lut = _REF_LUT.setdefault(bins, F.build_lut(bins))
+    t0 = time.perf_counter()
+    stack = F.build_integral_stack(F.gradient_map(F.Image(frame), lut))
+    g = F.DescriptorGeometry(64, 128, 8, block=1, block_stride=1, bins=bins, normalization=norm)
+    if scored:
+        F.scan(stack, F.LinearModel(g, np.asarray(w, dtype=np.float64), float(b)), stride,
+               float("-inf"))
+    else:
+        for _ in F.scan_descriptors(stack, g, stride):
+            pass
+    return time.perf_counter() - t0
+
+
+_REF_LUT: dict = {}
+
+
+def python_reference_sample(cfg, frames, seconds=6.0):
+    """The real Python reference (baseline/_ref, vendored by pip from
+    /root/reference) timed on a few frames: one process, then one frame per
+    host core in a process pool (OPENBLAS_NUM_THREADS=1).  Absent on the box
+    -> reported as unavailable."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "fasthog")):
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref)"}
+    if cfg.pyramid_step:
+        return {"unavailable": "one 8K frame's 20-level pyramid takes ~130 s in the Python "
+                               "reference (SURVEY 8a-13); not sampled"}
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from paper_1703_06256_b200 import synth
+
+    w, b = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
+    job = lambda f: (f, cfg.key, cfg.bins, cfg.stride, cfg.normalization, cfg.scored, w, b)  # noqa: E731
+    t, k = 0.0, 0
+    while k == 0 or (t < seconds / 2 and k < len(frames)):
+        t += _ref_frame(job(frames[k % len(frames)]))
+        k += 1
+    one = k * cfg.height * cfg.width / t / 1e6
+    out = {"one_process_mpx_s": one, "one_process_frames": k, "one_process_s": t}
+    try:
+        import multiprocessing as mp
+
+        procs = host_threads()
+        jobs = [job(frames[i % len(frames)]) for i in range(procs)]
+        ctx = mp.get_context("fork")
+        with ctx.Pool(procs) as pool:
+            pool.map(_ref_frame, jobs[:procs])  # warm: imports + LUT per worker
+            t0 = time.perf_counter()
+            pool.map(_ref_frame, jobs)
+            wall = time.perf_counter() - t0
+        out.update({"pool_mpx_s": procs * cfg.height * cfg.width / wall / 1e6,
+                    "pool_processes": procs, "pool_frames": procs, "pool_s": wall})
+    except Exception as exc:  # pragma: no cover - pool failures only lose the sample
+        out["pool_error"] = str(exc)[:200]
+    out["api"] = ("fasthog gradient_map -> build_integral_stack -> "
+                  + ("scan(threshold=-inf)" if cfg.scored else "scan_descriptors drained"))
+    return out
+
+
 def cpu_baseline(cfg, seconds, frames=None):
     """The oracle port on the host cores over a bounded sample of the workload
     (`frames`, if given, are the benchmark's own frames: no regeneration)."""
@@ -222,13 +348,28 @@ def cpu_baseline(cfg, seconds, frames=None):
             "sample": f"{passes} pass(es) over {count} {cfg.key} frames ({cfg.frames} per step) "
                       f"(oracle/hog_oracle.c, {threads} threads, {dt:.1f} s; 1 frame on 1 thread: "
                       f"{t1 * 1e3:.0f} ms)",
-            "single_thread_mpx_s": cfg.height * cfg.width / t1 / 1e6}
+            "single_thread_mpx_s": cfg.height * cfg.width / t1 / 1e6,
+            "host": host_info(),
+            "python_reference": python_reference_sample(cfg, frames if frames is not None else probe)}
+
+
+def global_frames(args, cfg, world: int) -> tuple[int, str]:
+    """(frames in the whole job's batch, scaling).  Strong scaling needs a
+    frame per rank; a batch smaller than the world (c1: one frame) runs weak."""
+    scaling = args.scaling
+    if scaling == "strong" and (args.frames or cfg.frames) < world:
+        scaling = "weak"
+    if scaling == "weak":
+        return world * (args.frames or cfg.frames), scaling
+    return args.frames or cfg.frames, scaling
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
+    nf_global, scaling = global_frames(args, cfg, world)
     threads = host_threads()
     probe = gen_frames(cfg, 0, 1)
     # each step: a bounded sample sized for ~3 s of all-core CPU work
@@ -242,15 +383,21 @@ def run_reference(args, cfg):
     value = px / (ms / 1e3) / 1e6
     line = {
         "impl": "reference", "metric": "Mpixel/s (LUT binning + per-bin integral planes + window HOG)",
-        "value": value, "unit": "Mpixel/s", "n_gpus": args.gpus, "steps": args.steps,
+        "value": value, "unit": "Mpixel/s (source pixels)" if cfg.pyramid_step else "Mpixel/s",
+        "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": workload_name(cfg), "frames_per_step": per_step,
-                   "implementation": "reference algorithm restated in C (oracle/, pinned to "
-                                     "the reference's golden vectors), all host threads"},
+        "scaling": scaling, "vs_baseline": None,
+        "dtype": "int32" if not cfg.scored else "int32+f64", "data": "synthetic",
+        "config": bench_config(cfg, nf_global, world, scaling,
+                               len(shard_frames(nf_global, 0, world, scaling))),
+        "reference": {"frames_per_step": per_step,
+                      "implementation": "reference algorithm restated in C (oracle/, pinned to "
+                                        "the reference's golden vectors), all host threads; "
+                                        "rank 0 only"},
         "cpu_baseline": {"value": value, "unit": "Mpixel/s", "cores": threads, "kind": "port",
                          "sample": f"{per_step} of {cfg.frames} {cfg.key} frames per step"},
-        "e2e": {"value": value, "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+        "e2e": {"value": value, "unit": "Mpixel/s (source pixels)" if cfg.pyramid_step else "Mpixel/s",
+                "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -304,13 +451,28 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.tolist()
 
-    nf = args.frames or cfg.frames
-    first = sharding.shard(rank, world, nf).start  # each rank: its own shard of distinct frames
-    frames = gen_frames(cfg, first, nf)
+    if args.split_frame:
+        return bench_split_frame(args, cfg, dev, world, rank, local, barrier, max_over_ranks,
+                                 backend)
+    nf_global, scaling = global_frames(args, cfg, world)
+    if args.shard_of > 1:  # diagnostic: one rank's shard of a W-way split, on this GPU
+        if world > 1:
+            raise SystemExit("--shard-of is a one-process diagnostic")
+        mine = sharding.split(nf_global, 0, args.shard_of)
+    else:
+        mine = shard_frames(nf_global, rank, world, scaling)
+    nf, first = len(mine), mine.start  # this rank's contiguous shard of the batch
+    frames = gen_frames(cfg, first, nf)  # frame i always comes from seed (config, i)
     weights, bias = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
+    job = {"nf_global": nf_global if args.shard_of <= 1 else nf, "scaling": scaling,
+           "mine": mine, "config": bench_config(cfg, nf_global, world, scaling, nf)}
+    if args.shard_of > 1:
+        job["config"]["shard_of"] = (f"diagnostic: rank 0's {nf}-frame shard of a {args.shard_of}-way "
+                                     f"split of {nf_global} frames, run alone on one GPU; value "
+                                     f"counts the shard's pixels only")
     if cfg.pyramid_step:
         return bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
-                             barrier, max_over_ranks)
+                             barrier, max_over_ranks, job)
     p = H.HogPipeline(nf, cfg.channels, cfg.height, cfg.width, cfg.bins, stride=cfg.stride,
                       normalization=cfg.normalization, weights=weights, bias=bias, device=dev,
                       chunks=args.chunks or None)
@@ -380,7 +542,7 @@ def main():
     plane_ms = sum(e0.elapsed_time(e1) for step_ev in pev for e0, e1 in step_ev) / K
     total_ms, plane_ms = max_over_ranks([total_ms, plane_ms])
     ms_per_step = total_ms / K
-    px_step = world * nf * cfg.height * cfg.width
+    px_step = job["nf_global"] * cfg.height * cfg.width  # the whole job's batch
     value = px_step / (ms_per_step / 1e3) / 1e6
 
     # diagnostic (outside the timed region): one more batch with per-stage events
@@ -404,7 +566,7 @@ def main():
     if not args.no_e2e:
         e2e = run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier,
                       args.e2e_chunk, args.e2e_slots, not args.no_graph, args.e2e_tail,
-                      bool(args.e2e_overlap))
+                      bool(args.e2e_overlap), job=job, rank=rank, dump=args.dump_result)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -414,14 +576,12 @@ def main():
         line = {
             "metric": "Mpixel/s (LUT binning + per-bin integral planes + window HOG)",
             "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "int32" if not cfg.scored else "int32+f64",
             "data": "synthetic",
-            "config": {"workload": workload_name(cfg), "frames_per_gpu": nf,
-                       "global_frames": world * nf,
-                       "parallelism": f"frame-sharded x{world}, no collective",
-                       "l2": f"inputs larger than L2 ({step_bytes / 1e9:.2f} GB compulsory "
-                             f"traffic per GPU per step vs 126 MB L2)",
+            "config": job["config"],
+            "diagnostics": {"shard_frames": [mine.start, mine.stop],
+                       "compulsory_gb_per_gpu_step": step_bytes / 1e9,
                        "k_planes_ms_per_step": plane_ms,
                        "stages_ms_diagnostic": stages_ms,
                        "chunks": nch, "cuda_graph": not args.no_graph,
@@ -454,8 +614,75 @@ def main():
     return 0
 
 
+def bench_split_frame(args, cfg, dev, world, rank, local, barrier, max_over_ranks, backend):
+    """One frame over `world` ranks: rank r bins its row slab
+    (+ halo rows), counts its rows' bins per column, one all_gather of those
+    counts (N_b x W int32 per rank, NCCL over NVLink) gives the carry from the
+    slabs above, then planes + cell-grid rows.  Per-frame latency = slowest
+    rank, every step bracketed by the exchange."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_1703_06256_b200 import slab, synth
+    from paper_1703_06256_b200.errors import PathMismatch
+
+    frame = synth.make_batch(cfg, 0, 1)
+    group = dist.group.WORLD if world > 1 else None
+    sp = slab.SlabPipeline(1, cfg.channels, cfg.height, cfg.width, cfg.bins, stride=cfg.stride,
+                           rank=rank, world=world, group=group, device=dev)
+    sp.upload(frame)
+    sp.run()
+    torch.cuda.synchronize()
+    # parity gate: this rank's cell-grid rows against the oracle's whole-frame grid
+    _, g_ref, _ = O.run_batch(frame, O.build_lut(cfg.bins), cfg.bins, 8, 64, 128, cfg.stride, 0,
+                              threads=host_threads(), want_outputs=True)
+    got = sp.grid_view()[0].cpu().numpy().astype(np.int64)
+    ok = np.array_equal(got, g_ref[0, sp.cell_row0: sp.cell_row0 + sp.ncy])
+    if max_over_ranks([0.0 if ok else 1.0])[0] != 0.0:
+        raise PathMismatch("slab cell grid differs from the oracle; refusing to time")
+    K, W = args.steps, args.warmup
+    for _ in range(W):
+        sp.run()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(K):
+        sp.run()
+    t1.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = max_over_ranks([t0.elapsed_time(t1) / K])[0]
+    barrier()
+    if rank == 0:
+        px = cfg.height * cfg.width
+        line = {
+            "metric": "Mpixel/s (LUT binning + per-bin integral planes + window HOG)",
+            "value": px / (ms / 1e3) / 1e6, "unit": "Mpixel/s", "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"split-frame: 1 frame of {workload_name(cfg)}",
+                       "global_frames": 1, "frames_per_gpu": 1, "scaling": "strong",
+                       "parallelism": f"one frame in {world} row slab(s); one all_gather of "
+                                      f"{cfg.bins}x{cfg.width} int32 column counts per rank "
+                                      f"({'nccl' if backend == 'nccl' else backend})",
+                       "l2": "frame planes larger than L2"},
+            "diagnostics": {"slab_rows": [sp.y0, sp.y1], "exchange_bytes_per_rank":
+                            4 * cfg.bins * cfg.width, "latency_ms_per_frame": ms},
+            "e2e": None, "cpu_baseline": None, "gpu_launches": 4 * K, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local, barrier,
-                  max_over_ranks):
+                  max_over_ranks, job):
     """Config c5: every frame scanned over its 20-level pyramid (detector.py:224-269).
     Mpixel/s counts source pixels; pyramid-level pixels are reported beside."""
     import torch
@@ -532,11 +759,12 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
         sp_gbs = sum(b for _, _, b in sev) / (sp_ms / 1e3) / 1e9
         serial = {"step_ms": s0.elapsed_time(s1), "k_planes_ms": sp_ms, "k_planes_gbs": sp_gbs,
                   "k_planes_frac": sp_gbs / measured_peak()[0]}
-    src_px = world * nf * cfg.height * cfg.width
-    lvl_px = world * nf * p.pixels_per_frame()
+    src_px = job["nf_global"] * cfg.height * cfg.width
+    lvl_px = job["nf_global"] * p.pixels_per_frame()
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier)
+        e2e = run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier,
+                              job=job, rank=rank, dump=args.dump_result)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, args.cpu_seconds, frames)
@@ -548,15 +776,15 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
             "metric": "Mpixel/s (LUT binning + per-bin integral planes + window HOG)",
             "value": src_px / (ms / 1e3) / 1e6, "unit": "Mpixel/s (source pixels)",
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": job["scaling"], "vs_baseline": None,
             "dtype": "int32+f64", "data": "synthetic",
-            "config": {"workload": workload_name(cfg), "frames_per_gpu": nf,
+            "config": job["config"],
+            "diagnostics": {"shard_frames": [job["mine"].start, job["mine"].stop],
                        "levels": len(p.levels), "level_mpixel_per_s": lvl_px / (ms / 1e3) / 1e6,
                        "frames_per_chunk": p.chunk, "level_streams": p.streams,
                        "band_rows_per_level": [q.band_rows for q in p.pipes],
                        "one_stream_diagnostic": serial,
-                       "parallelism": f"frame-sharded x{world}, no collective",
-                       "l2": f"inputs larger than L2 ({step_bytes / 1e9:.1f} GB per GPU per step)"},
+                       "compulsory_gb_per_gpu_step": step_bytes / 1e9},
             "roofline": {"bound": "hbm", "kernel": "k_planes", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                          "traffic_level0": {
@@ -578,7 +806,8 @@ def bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
     return 0
 
 
-def run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier):
+def run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, job=None,
+                    rank=0, dump=""):
     """c5 end to end through PyramidPipeline: per step, H2D of every source
     frame from pinned host memory (one copy per frame chunk on a copy stream;
     chunk j's levels start when its frames have landed) and D2H of every
@@ -588,7 +817,10 @@ def run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrie
     import torch
 
     host_in = torch.from_numpy(frames).pin_memory()
-    host_out = [torch.empty(tuple(s.shape), dtype=s.dtype).pin_memory() for s in p.scores]
+    # every level's score maps of the whole batch, one node-wide host buffer per level
+    gathers = [open_gather(job, s.shape[1:], s.dtype, rank, barrier, tag=f"lvl{i}")
+               for i, s in enumerate(p.scores)]
+    host_out = [gth.local() for gth in gathers]
     cin, cout = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     src = p.src.data
 
@@ -641,17 +873,39 @@ def run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrie
     torch.cuda.synchronize()
     ms = max_over_ranks([t0.elapsed_time(t1) / K])[0]
     ok = all(torch.equal(h, s.cpu()) for h, s in zip(host_out, p.scores))
-    return {"value": world * nf * cfg.height * cfg.width / (ms / 1e3) / 1e6,
+    ok = max_over_ranks([0.0 if ok else 1.0])[0] == 0.0
+    barrier()  # every shard's score maps are in the shared buffers
+    if dump and rank == 0:
+        np.savez(dump, *[gth.array for gth in gathers])
+    d2h = int(sum(h.numel() * h.element_size() for h in host_out))
+    for gth in gathers:
+        gth.close()
+    return {"value": job["nf_global"] * cfg.height * cfg.width / (ms / 1e3) / 1e6,
             "unit": "Mpixel/s (source pixels)", "ms_per_step": ms,
             "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
-            "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in host_out)),
+            "d2h_bytes_per_step": d2h,
+            "gather": "each rank's score maps land in its slices of node-wide page-locked host "
+                      "buffers (/dev/shm, cudaHostRegister), one per level, in frame order",
             "result": "window scores of every pyramid level", "chunk_frames": p.chunk,
             "streams": "1 H2D + 4 level streams + 1 D2H", "cuda_graph": False,
             "steps_overlap": True, "matches_device_run": ok}
 
 
+def open_gather(job, res_shape, dtype, rank, barrier, tag=""):
+    """The job's result buffer: one host array for the whole batch (frame
+    order) shared by the node's ranks; this rank writes its shard's slice."""
+    import torch
+
+    from paper_1703_06256_b200 import sharding
+
+    np_dtype = torch.empty((), dtype=dtype).numpy().dtype
+    run = os.environ.get("MASTER_PORT") if int(os.environ.get("WORLD_SIZE", "1")) > 1 else os.getpid()
+    return sharding.HostGather(f"{run}_{tag}", (job["nf_global"],) + tuple(res_shape), np_dtype,
+                               job["mine"], rank, barrier)
+
+
 def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, chunk=64, nslots=2,
-            use_graph=True, tail=1, overlap=True):
+            use_graph=True, tail=1, overlap=True, job=None, rank=0, dump=""):
     """Per step: H2D of every frame from pinned host memory, the pipeline, and
     D2H of the step's result, in frame chunks.  Each direction has ONE copy
     stream, so chunks cross PCIe in order at full bandwidth (copies issued on
@@ -689,7 +943,8 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
         a += sz
     host_in = torch.from_numpy(frames).pin_memory()
     res = jobs[0][2].result()
-    host_out = torch.empty((nf,) + tuple(res.shape[1:]), dtype=res.dtype).pin_memory()
+    gather = open_gather(job, res.shape[1:], res.dtype, rank, barrier)
+    host_out = gather.local()  # this shard's slice of the node-wide result buffer
 
     def steps(nsteps):
         """nsteps e2e steps.  Buffer reuse is guarded per pipeline (frames buffer
@@ -754,9 +1009,19 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
     ms = max_over_ranks([t0.elapsed_time(t1) / K])[0]
     # the D2H result must equal the device-resident run's result
     ok = bool(torch.equal(host_out.to(dev), p.result().to(host_out.dtype)))
-    return {"value": world * nf * cfg.height * cfg.width / (ms / 1e3) / 1e6, "unit": "Mpixel/s",
+    ok = max_over_ranks([0.0 if ok else 1.0])[0] == 0.0
+    barrier()  # every shard has landed in the shared buffer: rank 0 holds the whole batch
+    if dump and rank == 0:
+        np.save(dump, gather.array)
+    gather.close()
+    return {"value": job["nf_global"] * cfg.height * cfg.width / (ms / 1e3) / 1e6,
+            "unit": "Mpixel/s",
             "ms_per_step": ms, "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
             "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
+            "gather": (f"each rank's D2H lands in its slice of one {gather.nbytes / 1e6:.1f} MB "
+                       "page-locked host buffer shared by the node's ranks (/dev/shm, "
+                       "cudaHostRegister): the batch's results in frame order on the host"),
+            "bytes_per_gpu": "h2d/d2h bytes are this rank's shard",
             "result": "cell grid" if not cfg.scored else "window scores",
             "chunk_frames": sizes, "buffer_sets": nslots,
             "streams": "1 H2D + 1 compute + 1 D2H (in-order copies)", "cuda_graph": bool(use_graph),

@@ -31,3 +31,79 @@ def max_over_ranks(values, device=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.tolist()
+
+
+class HostGather:
+    """The batch's results in ONE host buffer shared by the ranks of a node
+    ("results are gathered to the host", no collective).
+
+    Rank 0 creates a file in /dev/shm sized for the whole batch; every rank
+    maps it and copies its own contiguous shard's results (device-to-host)
+    straight into its slice, so after a barrier rank 0 holds the batch's
+    results in frame order.  With CUDA the mapping is page-locked
+    (cudaHostRegister), so those copies are asynchronous DMA like any
+    pinned-buffer copy.  `rows` is this rank's range of the leading axis.
+    """
+
+    def __init__(self, tag: str, shape, dtype, rows: range, rank: int, barrier, pin: bool = True):
+        import mmap
+        import os
+
+        import numpy as np
+
+        self.rank = rank
+        self.shape, self.dtype = tuple(int(s) for s in shape), np.dtype(dtype)
+        self.nbytes = int(np.prod(self.shape, dtype=np.int64)) * self.dtype.itemsize
+        self.path = f"/dev/shm/hogb200_{tag}"
+        if rank == 0:
+            with open(self.path, "wb") as f:
+                f.truncate(max(self.nbytes, 1))
+        barrier()
+        fd = os.open(self.path, os.O_RDWR)
+        try:
+            self._mm = mmap.mmap(fd, max(self.nbytes, 1), mmap.MAP_SHARED,
+                                 mmap.PROT_READ | mmap.PROT_WRITE)
+        finally:
+            os.close(fd)
+        self.array = np.frombuffer(self._mm, dtype=self.dtype,
+                                   count=int(np.prod(self.shape, dtype=np.int64))).reshape(self.shape)
+        self.rows = rows
+        self._registered = False
+        self._barrier = barrier
+        if pin:
+            import torch
+
+            if torch.cuda.is_available() and self.nbytes:
+                ptr = self.array.ctypes.data
+                err = torch.cuda.cudart().cudaHostRegister(ptr, self.nbytes, 0)
+                if int(err) != 0:
+                    raise RuntimeError(f"cudaHostRegister failed ({err})")
+                self._registered = True
+        import torch
+
+        self.tensor = torch.from_numpy(self.array)  # whole batch (host)
+
+    def local(self):
+        """This rank's slice (a host tensor view of the shared buffer)."""
+        return self.tensor[self.rows.start: self.rows.stop]
+
+    def close(self):
+        """Unpin and unmap; rank 0 removes the file after every rank is done."""
+        import os
+
+        if self._registered:
+            import torch
+
+            torch.cuda.cudart().cudaHostUnregister(self.array.ctypes.data)
+            self._registered = False
+        del self.tensor, self.array
+        try:
+            self._mm.close()
+        except BufferError:  # views still held by the caller: unmapped when they go
+            pass
+        self._barrier()
+        if self.rank == 0:
+            try:
+                os.unlink(self.path)
+            except FileNotFoundError:
+                pass

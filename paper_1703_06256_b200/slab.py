@@ -129,14 +129,20 @@ class SlabPipeline:
         return self.own
 
     def exchange(self):
-        """Phase 2: base = sum of the own counts of the ranks above (one all_gather)."""
+        """Phase 2: base = sum of the own counts of the ranks above (one all_gather:
+        NCCL over NVLink on device buffers; a gloo group exchanges host copies)."""
         import torch.distributed as dist
 
-        parts = [D.torch().empty_like(self.own) for _ in range(self.world)]
-        dist.all_gather(parts, self.own, group=self.group)
-        self.base.zero_()
-        for r in range(self.rank):
-            self.base += parts[r]
+        t = D.torch()
+        on_dev = dist.get_backend(self.group) == "nccl"
+        own = self.own if on_dev else self.own.cpu()
+        parts = [t.empty_like(own) for _ in range(self.world)]
+        dist.all_gather(parts, own, group=self.group)
+        if self.rank == 0:
+            self.base.zero_()
+        else:
+            above = t.stack(parts[: self.rank]).sum(0, dtype=t.int32)
+            self.base.copy_(above, non_blocking=on_dev)
 
     def planes_and_grid(self, base=None, stream=None):
         """Phase 3: planes (global rows y0 .. y1e) and the owned grid rows."""

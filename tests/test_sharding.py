@@ -62,3 +62,38 @@ def test_gloo_two_ranks_shard_and_max():
     assert out[0][0] == synth.batch_sha256(full[:2])
     assert out[1][0] == synth.batch_sha256(full[2:])
     assert not np.array_equal(full[0], full[2])
+
+
+def _gather_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 7
+        mine = sharding.split(n, rank, world)
+        g = sharding.HostGather(f"test_{port}", (n, 3, 2), np.float64, mine, rank, dist.barrier,
+                                pin=False)
+        # each rank writes only its own contiguous slice
+        loc = g.local()
+        assert loc.shape[0] == len(mine)
+        for j, f in enumerate(mine):
+            loc[j] = float(f) + 0.25
+        dist.barrier()
+        if rank == 0:
+            out["gathered"] = g.array.copy()
+        g.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_host_gather_in_frame_order():
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gather_worker, args=(world, port, out), nprocs=world, join=True)
+    want = np.broadcast_to((np.arange(7) + 0.25)[:, None, None], (7, 3, 2))
+    assert np.array_equal(out["gathered"], want)
+    assert not os.path.exists(f"/dev/shm/hogb200_test_{port}")  # rank 0 removed the buffer
