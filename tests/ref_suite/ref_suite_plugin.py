@@ -41,7 +41,16 @@ fasthog.bench = _bench
 fasthog.run_bench = _bench.run_bench
 
 # nodeid suffix -> why the reference's assertion does not apply
-DIFFERS = {}
+DIFFERS = {
+    # detector.py:148 compares scan's score with np.dot(w, d) + b for EXACT equality;
+    # np.dot is OpenBLAS ddot, whose summation order is library- and CPU-defined
+    # (DYNAMIC_ARCH kernels), so no other summation reproduces it bit for bit.  The
+    # device sums the same products in fp64 in its own order: measured |diff| 7e-15
+    # on a score of 3.97 (relative 2e-15); the north star's bar is 1e-5 relative,
+    # which test_gpu_parity.py and test_gpu_c5_full.py check against the oracle.
+    "test_detector.py::test_scan_matches_naive_recompute":
+        "fp64 summation order differs from OpenBLAS ddot (relative error ~1e-15)",
+}
 
 
 def pytest_collection_modifyitems(config, items):
