@@ -212,14 +212,54 @@ bool v8_ok(const PlaneOut &po, const int8_t *bm, int64_t bp, int64_t bfs) {
     return po.vec && ((uintptr_t)bm & 7) == 0 && bp % 8 == 0 && bfs % 8 == 0;
 }
 
+// N_b > 18: groups of <= 16 consecutive bins, each through the single-write
+// plane kernel on a bin-offset copy of the bin map (k_bin_offset)
+constexpr int GROUP_BINS = 16;
+inline int bin_groups(int bins) { return (bins + GROUP_BINS - 1) / GROUP_BINS; }
+inline int group_range(int bins, int gi, int *b0) {
+    const int ng = bin_groups(bins), base = bins / ng, rem = bins % ng;
+    *b0 = gi * base + (gi < rem ? gi : rem);
+    return base + (gi < rem ? 1 : 0);
+}
+inline int64_t group_bm_pitch(int w) { return round_up(w, 8); }
+inline size_t group_bm_bytes(int n, int h, int w) {
+    return (size_t)round_up((int64_t)n * h * group_bm_pitch(w), 256);
+}
+
+int integral_group_impl(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w, int bins,
+                        int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, void *scratch,
+                        size_t sbytes, cudaStream_t st) {
+    const int64_t op = group_bm_pitch(w), ofs = (int64_t)h * op;
+    const size_t tb = group_bm_bytes(n, h, w);
+    if (scratch == nullptr || sbytes < tb)
+        return fail(HOG_EINVAL, "scratch too small: need more than %zu bytes, got %zu", tb, sbytes);
+    int8_t *tmp = (int8_t *)scratch;
+    void *rest = (char *)scratch + tb;
+    for (int gi = 0; gi < bin_groups(bins); ++gi) {
+        int b0;
+        const int nb = group_range(bins, gi, &b0);
+        PlaneOut po = make_po(pl + (int64_t)b0 * pns, pp, pns, pfs, w);
+        TileGeom g = make_geom(n, h, w, nb, false, 0, 0, v8_ok(po, tmp, op, ofs), po.vec != 0);
+        Scratch sc{};
+        const size_t need = carve(g, nullptr, nullptr);
+        if (sbytes < tb + need)
+            return fail(HOG_EINVAL, "scratch too small: need %zu bytes, got %zu", tb + need, sbytes);
+        carve(g, rest, &sc);
+        launch_bin_offset(bm, bp, bfs, n, h, w, b0, tmp, op, ofs, st);
+        GridOut go{nullptr, 4, 4, 1, 1, 0};
+        launch_counts_from_bm(g.NW, tmp, op, ofs, g, sc, st);
+        launch_scan(g.NW, g, sc, st);
+        launch_planes(g.NW, 0, 0, tmp, op, ofs, po, go, g, sc, FusedIn{}, st);
+    }
+    return check_launch("hog_integral (bin groups)");
+}
+
 int integral_impl(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w, int bins,
                   int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, void *scratch, size_t sbytes,
                   cudaStream_t st) {
     PlaneOut po = make_po(pl, pp, pns, pfs, w);
-    if (bins > MAX_FUSED_BINS) {
-        launch_generic_integral(bm, bp, bfs, po, n, h, w, bins, st);
-        return check_launch("integral (generic)");
-    }
+    if (bins > MAX_FUSED_BINS)
+        return integral_group_impl(bm, bp, bfs, n, h, w, bins, pl, pp, pns, pfs, scratch, sbytes, st);
     TileGeom g = make_geom(n, h, w, bins, false, 0, 0, v8_ok(po, bm, bp, bfs), po.vec != 0);
     Scratch sc{};
     size_t need = carve(g, nullptr, nullptr);
@@ -267,6 +307,17 @@ size_t hog_scratch_bytes(int n, int h, int w, int bins, int stride, int cell) {
     if (n < 1 || h < 1 || w < 1 || bins < 1) return 0;
     bool fused = stride > 0 && cell > 0;
     size_t m = 0;
+    if (bins > MAX_FUSED_BINS) {  // hog_integral in bin groups: offset bin map + a group's scratch
+        for (int gi = 0; gi < bin_groups(bins); ++gi) {
+            int b0;
+            const int nb = group_range(bins, gi, &b0);
+            for (int v8 = 0; v8 < 2; ++v8) {
+                const size_t a = carve(make_geom(n, h, w, nb, false, 0, 0, v8, true), nullptr, nullptr);
+                m = a > m ? a : m;
+            }
+        }
+        return group_bm_bytes(n, h, w) + m;
+    }
     for (int v8 = 0; v8 < 2; ++v8) {
         for (int tma = 0; tma < 2; ++tma) {
             size_t a = carve(make_geom(n, h, w, bins, fused, stride, cell, v8, tma), nullptr, nullptr);

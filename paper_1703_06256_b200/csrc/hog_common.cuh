@@ -331,8 +331,8 @@ inline void launch_planes(int nw, int kr, int ch, const int8_t *bm, int64_t bp, 
     else launch_planes_d(nw, kr, ch, bm, bp, bfs, po, go, g, sc, fi, st);
 }
 // k_window.cu
-void launch_generic_integral(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po, int n,
-                             int h, int w, int bins, cudaStream_t st);
+void launch_bin_offset(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w, int b0,
+                       int8_t *out, int64_t op, int64_t ofs, cudaStream_t st);
 void launch_cell_grid(const int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, int n, int bins,
                       const int32_t *cxs, int ncx, const int32_t *cys, int ncy, int cell,
                       int32_t *grid, cudaStream_t st);

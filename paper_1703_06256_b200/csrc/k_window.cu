@@ -9,35 +9,23 @@ namespace hogb200 {
 // ---------------------------------------------------------------------------
 // Generic integral for bins > 18 (API completeness; the configs use 8/9/18):
 // row prefix per plane row, then column prefix in place.
-__global__ void k_generic_rows(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po,
-                               int n, int h, int w, int bins) {
+// Bin-group pass for N_b > 18 (hog_integral): the single-write plane kernel
+// handles <= 18 bins, so N_b bins run as groups of <= 16 consecutive bins, each
+// over a copy of the bin map with the group's first bin subtracted (per byte,
+// mod 256).  Bins of the group become 0 .. nb-1; every other byte (earlier
+// bins wrap to >= 192, NO_BIN 0xFF to >= 192, later bins to nb .. 63) lands
+// on a one-hot shift past the group's counters or in a padding slot that is
+// never widened or stored, so each group's planes are exactly the
+// reference's planes of those bins (integral.py:75-79).
+__global__ void k_bin_offset(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, int n, int h,
+                             int w4, uint32_t sub4, int8_t *__restrict__ out, int64_t op, int64_t ofs) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)n * bins * (h + 1)) return;
-    const int Y = (int)(i % (h + 1));
-    const int b = (int)((i / (h + 1)) % bins);
-    const int f = (int)(i / ((int64_t)(h + 1) * bins));
-    int32_t *rp = po.pl + (int64_t)f * po.pfs + (int64_t)b * po.pns + (int64_t)Y * po.pp;
-    rp[0] = 0;
-    int32_t run = 0;
-    const int8_t *src = bm + (int64_t)f * bfs + (int64_t)(Y - 1) * bp;
-    for (int X = 1; X <= w; ++X) {
-        if (Y > 0 && src[X - 1] == b) ++run;
-        rp[X] = run;
-    }
-}
-
-__global__ void k_generic_cols(PlaneOut po, int n, int h, int w, int bins) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)n * bins * (w + 1)) return;
-    const int X = (int)(i % (w + 1));
-    const int b = (int)((i / (w + 1)) % bins);
-    const int f = (int)(i / ((int64_t)(w + 1) * bins));
-    int32_t *cp = po.pl + (int64_t)f * po.pfs + (int64_t)b * po.pns + X;
-    int32_t run = 0;
-    for (int Y = 0; Y <= h; ++Y) {
-        run += cp[(int64_t)Y * po.pp];
-        cp[(int64_t)Y * po.pp] = run;
-    }
+    if (i >= (int64_t)n * h * w4) return;
+    const int c = (int)(i % w4);
+    const int64_t r = i / w4;
+    const int y = (int)(r % h), f = (int)(r / h);
+    const uint32_t v = __ldg(reinterpret_cast<const uint32_t *>(bm + f * bfs + y * bp) + c);
+    reinterpret_cast<uint32_t *>(out + f * ofs + y * op)[c] = __vsub4(v, sub4);
 }
 
 // ---------------------------------------------------------------------------
@@ -305,11 +293,11 @@ k_resize(const uint8_t *__restrict__ src, int c, int h, int w, int64_t sp, int64
 
 // ---- launchers ------------------------------------------------------------
 
-void launch_generic_integral(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po, int n,
-                             int h, int w, int bins, cudaStream_t st) {
-    k_generic_rows<<<blocks_for((int64_t)n * bins * (h + 1), 128), 128, 0, st>>>(bm, bp, bfs, po, n,
-                                                                               h, w, bins);
-    k_generic_cols<<<blocks_for((int64_t)n * bins * (w + 1), 128), 128, 0, st>>>(po, n, h, w, bins);
+void launch_bin_offset(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w, int b0,
+                       int8_t *out, int64_t op, int64_t ofs, cudaStream_t st) {
+    const int w4 = (w + 3) / 4;
+    k_bin_offset<<<blocks_for((int64_t)n * h * w4, 256), 256, 0, st>>>(
+        bm, bp, bfs, n, h, w4, (uint32_t)b0 * 0x01010101u, out, op, ofs);
 }
 
 void launch_cell_grid(const int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, int n, int bins,
