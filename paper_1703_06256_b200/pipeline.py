@@ -37,6 +37,9 @@ def on_device(fn):
     return wrap
 
 
+MAX_PIPELINE_BINS = 18  # hog_pipeline's fused limit; more bins run binning + hog_integral groups
+
+
 def regular_lattice(cell_xs, cell_ys, stride: int, cell: int, bins: int) -> bool:
     """True when hog_pipeline can emit the grid from the plane kernel."""
     if stride % 4 or stride > 240 or cell % stride or cell // stride > 2 or cell % 4 or bins > 18:
@@ -227,6 +230,8 @@ class HogPipeline:
             lib.hog_set_band_rows(0)
 
     def _pipeline_call(self, base, a, b, fr, bm, pl, scr, sb, stages, evs, stream):
+        if self.bins > MAX_PIPELINE_BINS:
+            return self._grouped_call(base, a, b, fr, bm, pl, scr, sb, stages, evs, stream)
         _native.call("hog_pipeline", base + a * fr.fstride, b - a, self.c, self.h,
                      self.w, fr.pitch, fr.cstride, fr.fstride, D.ptr(self.lut_dev), self.bins,
                      D.ptr(bm.data) + a * bm.fstride, bm.pitch, bm.fstride,
@@ -238,6 +243,22 @@ class HogPipeline:
                      D.stream_handle(stream))
 
     @on_device
+    def _grouped_call(self, base, a, b, fr, bm, pl, scr, sb, stages, evs, stream):
+        """N_b > 18 (hog_pipeline's fused limit): binning (hog_grad_bin), then the
+        planes in bin groups (hog_integral); the cell grid comes from
+        hog_cell_grid in _post (the lattice is not fused).  Stage events are not
+        recorded on this path (no BASELINE configuration has N_b > 18)."""
+        h = D.stream_handle(stream)
+        bmp = D.ptr(bm.data) + a * bm.fstride
+        if stages & _native.STAGE_BIN:
+            _native.call("hog_grad_bin", base + a * fr.fstride, b - a, self.c, self.h, self.w,
+                         fr.pitch, fr.cstride, fr.fstride, D.ptr(self.lut_dev), self.bins, bmp,
+                         bm.pitch, bm.fstride, h)
+        if stages & _native.STAGE_PLANES:
+            _native.call("hog_integral", bmp, b - a, self.h, self.w, bm.pitch, bm.fstride,
+                         self.bins, pl.ptr + 4 * a * pl.fstride, pl.pitch, pl.nstride, pl.fstride,
+                         D.ptr(scr), sb, h)
+
     def run(self, stream=None, plane_events=None, frames_ptr=None, scores_ptr=None,
             pipelined: bool = False):
         """Enqueue the whole batch; results are ready in `stream` order (default:
@@ -397,6 +418,8 @@ class HogPipeline:
 
     def launches_per_run(self) -> int:
         k = 3 * self.chunks  # grad_bin + carry scan + planes per chunk
+        if self.bins > MAX_PIPELINE_BINS:  # grad_bin + per bin group: offset, counts, scan, planes
+            k = (1 + 4 * -(-self.bins // 16)) * self.chunks
         post = (0 if self.fused else 1) + (1 if self.denom is not None else 0) + \
             (1 if self.scores is not None else 0)
         return k + post * self.chunks  # grid consumers run per chunk

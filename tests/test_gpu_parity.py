@@ -533,3 +533,32 @@ def test_big_batch_paths_vs_oracle(key, count):
     if cfg.scored:
         np.testing.assert_allclose(p.scores[ends].cpu().numpy(), scores, rtol=1e-9,
                                    atol=score_tol(weights))
+
+
+@pytest.mark.parametrize("bins,stride,norm", [(20, 8, "none"), (32, 4, "l2"), (64, 8, "none")])
+def test_pipeline_more_than_18_bins_vs_oracle(bins, stride, norm):
+    """N_b > 18: HogPipeline bins, then builds the planes in bin groups through the
+    single-write plane kernel (hog_integral) and the grid with hog_cell_grid."""
+    cfg = synth.CONFIGS["c2"]
+    frames = np.ascontiguousarray(synth.make_batch(cfg, 5, 3)[:, :, :200, :330])
+    rng = np.random.default_rng(bins)
+    w = rng.normal(0, 0.01, 128 * bins)
+    scored = norm == "none"
+    p = H.HogPipeline(3, 1, 200, 330, bins, stride=stride, normalization=norm,
+                      weights=w if scored else None, bias=0.25)
+    assert not p.fused
+    p.upload(frames)
+    p.run()
+    torch.cuda.synchronize()
+    lut = O.build_lut(bins)
+    for i in range(3):
+        cells = O.gradient_map(frames[i], lut)
+        assert np.array_equal(p.binmap_view()[i].cpu().numpy().astype(np.int16), cells)
+        assert np.array_equal(p.planes_view()[i].cpu().numpy().view(np.uint32),
+                              O.integral_stack(cells, bins))
+    mode = 1 if scored else 2
+    _, grid, scores = O.run_batch(frames, lut, bins, 8, 64, 128, stride, mode,
+                                  w if scored else None, 0.25, threads=2, want_outputs=True)
+    assert np.array_equal(p.grid.cpu().numpy().astype(np.int64), grid)
+    if scored:
+        np.testing.assert_allclose(p.scores.cpu().numpy(), scores, rtol=0, atol=score_tol(w))
