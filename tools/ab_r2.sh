@@ -7,19 +7,24 @@ O=gpurun_out
 V=()
 while [ "$1" != "--" ]; do V+=("$1"); shift; done
 shift
-for c in "$@"; do
+# a config may carry extra bench args after a colon: c2:--shard-of=8
+for spec_c in "$@"; do
+  c=${spec_c%%:*}; xargs_=""
+  [[ "$spec_c" == *:* ]] && xargs_=$(echo "${spec_c#*:}" | tr ',' ' ')
+  tagc=$(echo "$spec_c" | tr ':=,' '___')
   for rep in 1 2; do
     for i in "${!V[@]}"; do
       spec=${V[$i]}; lib=${spec%%@*}; envs=""
       [[ "$spec" == *@* ]] && envs=$(echo "${spec#*@}" | tr ',' ' ')
-      env HOGB200_LIB=$lib $envs python bench.py --config $c --steps 20 --warmup 5 --no-e2e \
-        --no-cpu-baseline > $O/ab_${c}_${i}_${rep}.json 2> $O/ab_${c}_${i}_${rep}.err
+      env HOGB200_LIB=$lib $envs python bench.py --config $c $xargs_ --steps 20 --warmup 5 --no-e2e \
+        --no-cpu-baseline > $O/ab_${tagc}_${i}_${rep}.json 2> $O/ab_${tagc}_${i}_${rep}.err
     done
   done
 done
 python - "${#V[@]}" "${V[@]}" -- "$@" <<'PY'
 import json, sys, glob
-n = int(sys.argv[1]); specs = sys.argv[2:2 + n]; cfgs = sys.argv[3 + n:]
+n = int(sys.argv[1]); specs = sys.argv[2:2 + n]
+cfgs = [c.replace(":", "_").replace("=", "_").replace(",", "_") for c in sys.argv[3 + n:]]
 for c in cfgs:
     for i, spec in enumerate(specs):
         for f in sorted(glob.glob(f"gpurun_out/ab_{c}_{i}_*.json")):
