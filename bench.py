@@ -56,6 +56,9 @@ def parse_args():
     ap.add_argument("--dump-result", default="",
                     help="rank 0 saves the gathered e2e result (whole batch, frame order) "
                          "to this .npy path")
+    ap.add_argument("--window-l2", action="store_true",
+                    help="EXTENSION for c3's wording: per-window L2 norms of the unnormalised "
+                         "window descriptors instead of the reference's per-cell (block=1) L2")
     ap.add_argument("--split-frame", action="store_true",
                     help="one frame of the config (c5: one 8K frame) cut into row slabs, one "
                          "per rank, with the column-carry all_gather (SURVEY 8f-2); reports "
@@ -84,11 +87,14 @@ def parse_args():
     return ap.parse_args()
 
 
-def workload_name(cfg) -> str:
+def workload_name(cfg, window_l2: bool = False) -> str:
     kind = "i.i.d. uniform noise" if cfg.sigma is None else f"blurred noise sigma={cfg.sigma}"
     extra = f" + {cfg.rects} rects" if cfg.rects else ""
     tail = ", linear score" if cfg.scored else ""
     norm = f", per-cell {cfg.normalization}" if cfg.normalization != "none" else ""
+    if window_l2:
+        norm = (", per-window l2 (EXTENSION: the reference normalises per block; checked against "
+                "a numpy restatement)")
     return (f"{cfg.key}: {cfg.frames}x {cfg.channels}x{cfg.height}x{cfg.width} u8 ({kind}{extra}), "
             f"N_b={cfg.bins}, cell 8, 64x128 windows stride {cfg.stride}{norm}{tail}")
 
@@ -466,6 +472,8 @@ def main():
     weights, bias = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
     job = {"nf_global": nf_global if args.shard_of <= 1 else nf, "scaling": scaling,
            "mine": mine, "config": bench_config(cfg, nf_global, world, scaling, nf)}
+    if args.window_l2:
+        job["config"]["workload"] = workload_name(cfg, window_l2=True)
     if args.shard_of > 1:
         job["config"]["shard_of"] = (f"diagnostic: rank 0's {nf}-frame shard of a {args.shard_of}-way "
                                      f"split of {nf_global} frames, run alone on one GPU; value "
@@ -474,8 +482,9 @@ def main():
         return bench_pyramid(args, cfg, frames, nf, weights, bias, dev, world, rank, local,
                              barrier, max_over_ranks, job)
     p = H.HogPipeline(nf, cfg.channels, cfg.height, cfg.width, cfg.bins, stride=cfg.stride,
-                      normalization=cfg.normalization, weights=weights, bias=bias, device=dev,
-                      chunks=args.chunks or None)
+                      normalization="none" if args.window_l2 else cfg.normalization,
+                      weights=weights, bias=bias, device=dev, chunks=args.chunks or None,
+                      window_norm="l2" if args.window_l2 else None)
     p.upload(frames)
     p.run()
     torch.cuda.synchronize()
@@ -484,7 +493,7 @@ def main():
     from oracle import oracle as O
 
     check = [0, nf - 1] if nf > 1 else [0]
-    mode = 1 if cfg.scored else (2 if cfg.normalization == "l2" else 0)
+    mode = 1 if cfg.scored else (2 if cfg.normalization == "l2" and not args.window_l2 else 0)
     _, g_ref, s_ref = O.run_batch(frames[check], O.build_lut(cfg.bins), cfg.bins, 8, 64, 128,
                                   cfg.stride, mode, weights, bias, threads=2, want_outputs=True)
     if not np.array_equal(p.grid[check].cpu().numpy().astype(np.int64), g_ref):
@@ -493,6 +502,13 @@ def main():
         s = p.scores[check].cpu().numpy()
         if (np.abs(s - s_ref) > 1e-5 * np.abs(s_ref) + 1e-12).any():
             raise PathMismatch("GPU scores differ from the oracle beyond 1e-5; refusing to time")
+    if args.window_l2:  # numpy restatement of the extension over the oracle's grid
+        for j, f in enumerate(check):
+            q = (g_ref[j] ** 2).sum(-1)
+            S = q[p.row_idx[:, None, :, None], p.col_idx[None, :, None, :]].sum((2, 3))
+            if not np.array_equal(p.window_norms[f].cpu().numpy(),
+                                  np.sqrt(S.astype(np.float64) + 1e-6 * 1e-6)):
+                raise PathMismatch("per-window L2 norms differ from the restatement")
 
     K, W = args.steps, args.warmup
     for _ in range(W):

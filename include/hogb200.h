@@ -231,6 +231,19 @@ int hog_detect(const double *scores, int n, int noy, int nox, double threshold,
 /* Scratch bytes for hog_nms over n detections. */
 size_t hog_nms_scratch_bytes(int n);
 
+/* EXTENSION (not a reference function): per-WINDOW L2 norms for BASELINE
+ * configs[2]'s "per-window L2 normalisation"; the reference normalises per
+ * block (descriptor.py:107-124).  norms[f][iy][ix] = sqrt(sum over the window's
+ * cells (row_idx[iy][0..cells_y) x col_idx[ix][0..cells_x)) of sum_b v^2 +
+ * eps_term), v the cell counts of `grid` ([n][ncy][ncx][bins], uint8 when
+ * elem_bytes == 1, int32 when 4); eps_term = _EPS*_EPS (descriptor.py:123).
+ * Bit-exact with np.sqrt((d*d).sum() + eps_term) of the window's unnormalised
+ * descriptor d.  cell_sq: caller scratch of n*ncy*ncx int32. */
+int hog_window_l2(const void *grid, int elem_bytes, int n, int ncy, int ncx, int bins,
+                  const int32_t *row_idx, int noy, const int32_t *col_idx, int nox, int cells_x,
+                  int cells_y, double eps_term, int32_t *cell_sq, double *norms,
+                  hog_stream_t stream);
+
 /* detector.py:285-299 (nms): greedy non-maximum suppression of n boxes
  * (x, y, w, h int32) with scores and scales (float64): candidates in order
  * of (-score, y, x, scale) (stable), a candidate is kept iff its IoU

@@ -65,6 +65,46 @@ __global__ void k_cell_norm(const int32_t *__restrict__ grid, int64_t ncells_tot
 }
 
 // ---------------------------------------------------------------------------
+// Per-WINDOW L2 norm (an extension for BASELINE configs[2]'s wording; the
+// reference normalises per block, descriptor.py:107-124): the norm of the
+// window's unnormalised descriptor d (its cells' histograms, descriptor.py:
+// 115-118) is sqrt(sum d^2 + eps^2), eps^2 = _EPS*_EPS as descriptor.py:123.
+// Counts are integers, so sum d^2 is exact in int64 and in fp64, and IEEE
+// sqrt makes the norm bit-exact with numpy's np.sqrt((d*d).sum() + _EPS*_EPS).
+// Pass 1: per-cell sum of squares; pass 2: one thread per window sums its cells.
+template <typename T>
+__global__ void k_cell_sq(const T *__restrict__ grid, int64_t ncells_total, int bins,
+                          int32_t *__restrict__ sq) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ncells_total) return;
+    const T *gp = grid + i * bins;
+    int32_t s = 0;
+    for (int b = 0; b < bins; ++b) {
+        const int32_t v = (int32_t)gp[b];
+        s += v * v;
+    }
+    sq[i] = s;
+}
+
+__global__ void k_window_l2(const int32_t *__restrict__ sq, int n, int ncy, int ncx,
+                            const int32_t *__restrict__ row_idx, int noy,
+                            const int32_t *__restrict__ col_idx, int nox, int cells_x, int cells_y,
+                            double eps_term, double *__restrict__ norms) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)n * noy * nox) return;
+    const int ix = (int)(i % nox);
+    const int64_t r = i / nox;
+    const int iy = (int)(r % noy), f = (int)(r / noy);
+    const int32_t *sf = sq + (int64_t)f * ncy * ncx;
+    int64_t s = 0;
+    for (int cy = 0; cy < cells_y; ++cy) {
+        const int32_t *row = sf + (int64_t)__ldg(row_idx + (int64_t)iy * cells_y + cy) * ncx;
+        for (int cx = 0; cx < cells_x; ++cx) s += __ldg(row + __ldg(col_idx + (int64_t)ix * cells_x + cx));
+    }
+    norms[i] = __dsqrt_rn(__dadd_rn((double)s, eps_term));
+}
+
+// ---------------------------------------------------------------------------
 // Window scores on a regular cell lattice (detector.py:140-154 with block = 1,
 // descriptor.py:107-124): the window at lattice origin (iy, ix) reads cells
 // (iy + cy*K, ix + cx*K), so scoring is a 2-D correlation of the cell grid
@@ -306,6 +346,19 @@ void launch_cell_grid(const int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, i
     k_cell_grid<<<blocks_for((int64_t)n * ncx * ncy, 128), 128, 0, st>>>(pl, pp, pns, pfs, n, bins,
                                                                          cxs, ncx, cys, ncy, cell,
                                                                          grid);
+}
+
+void launch_window_l2(const void *grid, int elem_bytes, int n, int ncy, int ncx, int bins,
+                      const int32_t *row_idx, int noy, const int32_t *col_idx, int nox, int cells_x,
+                      int cells_y, double eps_term, int32_t *sq, double *norms, cudaStream_t st) {
+    const int64_t cells = (int64_t)n * ncy * ncx;
+    if (elem_bytes == 1)
+        k_cell_sq<uint8_t><<<blocks_for(cells, 256), 256, 0, st>>>((const uint8_t *)grid, cells, bins, sq);
+    else
+        k_cell_sq<int32_t><<<blocks_for(cells, 256), 256, 0, st>>>((const int32_t *)grid, cells, bins, sq);
+    const int64_t tot = (int64_t)n * noy * nox;
+    k_window_l2<<<blocks_for(tot, 128), 128, 0, st>>>(sq, n, ncy, ncx, row_idx, noy, col_idx, nox,
+                                                      cells_x, cells_y, eps_term, norms);
 }
 
 void launch_cell_norm(const int32_t *grid, int64_t tot, int bins, int norm, double eps_term,

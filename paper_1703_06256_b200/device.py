@@ -4,7 +4,10 @@ allocations; the compute is libhogb200.so).
 HBM layouts (include/hogb200.h):
   frames  uint8 (N, C, H, Wp)        Wp = round_up(W, 4)   (pitched rows)
   binmap  int8  (N, H, Wb)           Wb = round_up(W, 8); -1 = NO_BIN
-  planes  int32 (N, bins, H+1, Pp)   Pp = round_up(W, 8) + 8; the tensor view
+  planes  int32 (N, H+1, bins, Pp)   Pp = round_up(W, 8) + 8 (row-major: the rows
+                                     of all bins for one plane row are adjacent;
+                                     HOGB200_PLANE_LAYOUT=bin gives (N, bins, H+1, Pp));
+                                     the view is the logical (N, bins, H+1, W+1) and
                                      starts 7 elements into its allocation so
                                      plane column 1 of every row is 32-byte
                                      aligned: each lane's 8 columns are one
@@ -121,21 +124,34 @@ def alloc_binmap(n, h, w, device=None) -> DevBinmap:
 
 @dataclass
 class DevPlanes:
+    """int32 planes of n frames: logical (n, bins, h+1, w+1), rows padded to
+    `rowlen` = hog_plane_pitch(w) elements.  Two HBM layouts, both addressed by
+    the C ABI through (pitch = row stride, nstride = bin stride, fstride =
+    frame stride) in elements:
+      bin-major   [n][bins][h+1][rowlen]   (the reference's (bins, H+1, W+1) order)
+      row-major   [n][h+1][bins][rowlen]   (a plane row of every bin is contiguous)
+    """
+
     base: object  # int32 allocation
     n: int
     bins: int
     h: int
     w: int
-    pitch: int
+    rowlen: int
     offset: int = 7
+    row_major: bool = False
 
     @property
-    def nstride(self) -> int:
-        return (self.h + 1) * self.pitch
+    def pitch(self) -> int:  # elements between plane rows Y and Y+1 of one bin
+        return self.bins * self.rowlen if self.row_major else self.rowlen
+
+    @property
+    def nstride(self) -> int:  # elements between bins
+        return self.rowlen if self.row_major else (self.h + 1) * self.rowlen
 
     @property
     def fstride(self) -> int:
-        return self.bins * self.nstride
+        return self.bins * (self.h + 1) * self.rowlen
 
     @property
     def ptr(self) -> int:
@@ -144,15 +160,31 @@ class DevPlanes:
     def view(self):
         """(N, bins, H+1, W+1) int32 strided view of the logical planes."""
         flat = self.base[self.offset: self.offset + self.n * self.fstride]
-        return flat.view(self.n, self.bins, self.h + 1, self.pitch)[..., : self.w + 1]
+        if self.row_major:
+            v = flat.view(self.n, self.h + 1, self.bins, self.rowlen).permute(0, 2, 1, 3)
+        else:
+            v = flat.view(self.n, self.bins, self.h + 1, self.rowlen)
+        return v[..., : self.w + 1]
 
 
-def alloc_planes(n, bins, h, w, device=None) -> DevPlanes:
+def plane_layout_row_major() -> bool:
+    """HBM layout of new plane buffers: row-major by default (a plane row of every
+    bin is one contiguous run, so the plane kernel's row writes stay in fewer DRAM
+    pages: measured on B200, c2 1.123 -> 1.110 ms, c4 2.149 -> 2.122 ms, the 64-frame
+    shard 0.181 -> 0.177 ms, c1/c3/c5 unchanged; profiles/r2/plane_layout_ab.md).
+    HOGB200_PLANE_LAYOUT=bin selects the reference's bin-major order."""
+    import os
+
+    return os.environ.get("HOGB200_PLANE_LAYOUT", "row") != "bin"
+
+
+def alloc_planes(n, bins, h, w, device=None, row_major=None) -> DevPlanes:
     t = require_cuda()
-    pitch = int(_native.load().hog_plane_pitch(w))
-    total = n * bins * (h + 1) * pitch + 16
+    rowlen = int(_native.load().hog_plane_pitch(w))
+    total = n * bins * (h + 1) * rowlen + 16
     base = t.empty(total, dtype=t.int32, device=device or "cuda")
-    return DevPlanes(base, n, bins, h, w, pitch)
+    rm = plane_layout_row_major() if row_major is None else bool(row_major)
+    return DevPlanes(base, n, bins, h, w, rowlen, row_major=rm)
 
 
 @dataclass

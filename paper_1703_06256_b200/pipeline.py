@@ -70,8 +70,18 @@ class HogPipeline:
     def __init__(self, n: int, channels: int, height: int, width: int, bins: int, *,
                  stride: int, cell: int = 8, window=(64, 128), normalization: str = "none",
                  weights=None, bias: float = 0.0, lut=None, device=None, chunks: int | None = None,
-                 grid_dtype: str = "auto", band_rows: int | None = None):
+                 grid_dtype: str = "auto", band_rows: int | None = None,
+                 window_norm: str | None = None):
+        """window_norm="l2" (an EXTENSION, not a reference behaviour): per-window L2
+        norms of the unnormalised window descriptors, for BASELINE configs[2]'s
+        "per-window L2 normalisation" (the reference normalises per block);
+        p.window_norms holds them and window_descriptors() divides by them."""
         t = D.require_cuda()
+        if window_norm not in (None, "l2"):
+            raise ValueError(f"window_norm must be None or 'l2', got {window_norm!r}")
+        if window_norm is not None and normalization != "none":
+            raise ValueError("window_norm applies to unnormalised cells (normalization='none')")
+        self.window_norm = window_norm
         self.n, self.c, self.h, self.w, self.bins = n, channels, height, width, bins
         self.stride, self.cell = stride, cell
         self.geometry = DescriptorGeometry(window[0], window[1], cell, block=1, block_stride=1,
@@ -130,8 +140,13 @@ class HogPipeline:
                 raise ValueError("weights length does not match the geometry")
             self.scores = t.empty((n, len(self.oys), len(self.oxs)), dtype=t.float64, device=dev)
             self.w_dev = t.as_tensor(self.weights, device=dev)
+        if self.weights is not None or window_norm is not None:
             self.ri_dev = t.as_tensor(self.row_idx.astype(np.int32), device=dev)
             self.ci_dev = t.as_tensor(self.col_idx.astype(np.int32), device=dev)
+        self.window_norms = None
+        if window_norm is not None:
+            self.window_norms = t.empty((n, len(self.oys), len(self.oxs)), dtype=t.float64, device=dev)
+            self.cell_sq = t.empty((n, self.ncy, self.ncx), dtype=t.int32, device=dev)
         self.band_rows_timings = None
         if band_rows is None and self.chunks == 1 and _tune_enabled():
             self.band_rows = self._tune_band_rows()
@@ -374,6 +389,12 @@ class HogPipeline:
         if self.denom is not None:
             _native.call("hog_cell_norm", gp, n, cells, self.bins, _NORM_CODE[g.normalization],
                          eps_term(g.normalization), dp, s)
+        if self.window_norms is not None:
+            _native.call("hog_window_l2", gp, self.grid.element_size(), n, self.ncy, self.ncx,
+                         self.bins, D.ptr(self.ri_dev), len(self.oys), D.ptr(self.ci_dev),
+                         len(self.oxs), g.cells_x, g.cells_y, eps_term("l2"),
+                         D.ptr(self.cell_sq) + 4 * a * cells, D.ptr(self.window_norms) + 8 * a * nwin,
+                         s)
         if self.scores is not None and self.fused and g.cells_x == 8 and self.grid_u8:
             _native.call("hog_scores_lattice_u8", gp, n, self.ncy, self.ncx,
                          self.bins, len(self.oys), len(self.oxs), g.cells_x, g.cells_y,
@@ -421,7 +442,7 @@ class HogPipeline:
         if self.bins > MAX_PIPELINE_BINS:  # grad_bin + per bin group: offset, counts, scan, planes
             k = (1 + 4 * -(-self.bins // 16)) * self.chunks
         post = (0 if self.fused else 1) + (1 if self.denom is not None else 0) + \
-            (1 if self.scores is not None else 0)
+            (1 if self.scores is not None else 0) + (2 if self.window_norms is not None else 0)
         return k + post * self.chunks  # grid consumers run per chunk
 
     # -- views ----------------------------------------------------------------
@@ -435,9 +456,28 @@ class HogPipeline:
         """The step's result tensor (what a caller reads back)."""
         if self.scores is not None:
             return self.scores
+        if self.window_norms is not None:
+            return self.window_norms
         if self.denom is not None:
             return self.denom
         return self.grid
+
+    def window_descriptors(self, frame: int, rows=None):
+        """EXTENSION (window_norm="l2"): per-window L2-normalised descriptors of window
+        rows `rows` (a slice; default all) of one frame, (rows, nox, D) float64 on the
+        device: the reference's unnormalised descriptor (descriptor.py:115-118) divided
+        by the window's norm (IEEE division, so equal to d / np.sqrt((d*d).sum() + eps^2))."""
+        if self.window_norms is None:
+            raise ValueError("window_descriptors needs window_norm='l2'")
+        from .descriptor import window_features_device
+
+        t = D.torch()
+        self.join()
+        rows = slice(None) if rows is None else rows
+        grid = self.grid[frame:frame + 1].to(t.int32)
+        _, desc = window_features_device(grid, self.geometry, self.row_idx[rows], self.col_idx,
+                                         want_desc=True)
+        return desc[0] / self.window_norms[frame, rows][..., None]
 
     def normalized_grid(self):
         """Per-cell normalised histograms (descriptor.py:119-124 with block=1)."""
@@ -452,6 +492,8 @@ class HogPipeline:
             b += 8 * len(self.oxs) * len(self.oys)
         if self.denom is not None:
             b += 8 * self.ncx * self.ncy
+        if self.window_norms is not None:
+            b += 8 * len(self.oxs) * len(self.oys)
         return b
 
     def plane_kernel_bytes_per_frame(self) -> int:
