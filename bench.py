@@ -926,7 +926,8 @@ def open_gather(job, res_shape, dtype, rank, barrier, tag=""):
     np_dtype = torch.empty((), dtype=dtype).numpy().dtype
     run = os.environ.get("MASTER_PORT") if int(os.environ.get("WORLD_SIZE", "1")) > 1 else os.getpid()
     return sharding.HostGather(f"{run}_{tag}", (job["nf_global"],) + tuple(res_shape), np_dtype,
-                               job["mine"], rank, barrier)
+                               job["mine"], rank, barrier,
+                               single_process=int(os.environ.get("WORLD_SIZE", "1")) == 1)
 
 
 def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, chunk=64, nslots=2,

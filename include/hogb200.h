@@ -238,10 +238,13 @@ size_t hog_nms_scratch_bytes(int n);
  * eps_term), v the cell counts of `grid` ([n][ncy][ncx][bins], uint8 when
  * elem_bytes == 1, int32 when 4); eps_term = _EPS*_EPS (descriptor.py:123).
  * Bit-exact with np.sqrt((d*d).sum() + eps_term) of the window's unnormalised
- * descriptor d.  cell_sq: caller scratch of n*ncy*ncx int32. */
+ * descriptor d.  k > 0: the lattice is regular (window (iy, ix) reads cells
+ * (iy + cy*k, ix + cx*k); the index maps are then not read) and the sums are
+ * separable; k = 0: the index maps give the cells.  cell_sq: caller scratch of
+ * n*ncy*ncx (+ n*ncy*nox when k > 0) int32. */
 int hog_window_l2(const void *grid, int elem_bytes, int n, int ncy, int ncx, int bins,
                   const int32_t *row_idx, int noy, const int32_t *col_idx, int nox, int cells_x,
-                  int cells_y, double eps_term, int32_t *cell_sq, double *norms,
+                  int cells_y, int k, double eps_term, int32_t *cell_sq, double *norms,
                   hog_stream_t stream);
 
 /* detector.py:285-299 (nms): greedy non-maximum suppression of n boxes

@@ -48,7 +48,7 @@ SIGNATURES = {
     "hog_nms_scratch_bytes": (_SZ, [_I]),
     "hog_nms": (_I, [_P, _P, _P, _I, _D, _P, _P, _P, _SZ, _P]),
     "hog_nms_f64": (_I, [_P, _P, _P, _I, _D, _P, _P, _P, _SZ, _P]),
-    "hog_window_l2": (_I, [_P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _I, _I, _D, _P, _P, _P]),
+    "hog_window_l2": (_I, [_P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _I, _I, _I, _D, _P, _P, _P]),
 }
 
 

@@ -497,14 +497,18 @@ int hog_cell_norm(const int32_t *grid, int n, int ncells, int bins, int norm, do
 
 int hog_window_l2(const void *grid, int elem_bytes, int n, int ncy, int ncx, int bins,
                   const int32_t *row_idx, int noy, const int32_t *col_idx, int nox, int cells_x,
-                  int cells_y, double eps_term, int32_t *cell_sq, double *norms, hog_stream_t stream) {
+                  int cells_y, int k, double eps_term, int32_t *cell_sq, double *norms,
+                  hog_stream_t stream) {
     g_err.clear();
     if (elem_bytes != 1 && elem_bytes != 4) return fail(HOG_EINVAL, "elem_bytes must be 1 or 4");
     if (n < 1 || ncy < 1 || ncx < 1 || bins < 1 || noy < 1 || nox < 1 || cells_x < 1 || cells_y < 1 ||
         !grid || !row_idx || !col_idx || !cell_sq || !norms)
         return fail(HOG_EINVAL, "bad arguments");
+    if (k > 0 && ((int64_t)(noy - 1) + (int64_t)(cells_y - 1) * k >= ncy ||
+                  (int64_t)(nox - 1) + (int64_t)(cells_x - 1) * k >= ncx))
+        return fail(HOG_EINVAL, "window grid exceeds the cell lattice");
     launch_window_l2(grid, elem_bytes, n, ncy, ncx, bins, row_idx, noy, col_idx, nox, cells_x, cells_y,
-                     eps_term, cell_sq, norms, (cudaStream_t)stream);
+                     k, eps_term, cell_sq, norms, (cudaStream_t)stream);
     return check_launch("hog_window_l2");
 }
 

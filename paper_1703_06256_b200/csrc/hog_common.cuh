@@ -340,7 +340,7 @@ void launch_cell_norm(const int32_t *grid, int64_t ncells_total, int bins, int n
                       double eps_term, double *den, cudaStream_t st);
 void launch_window_l2(const void *grid, int elem_bytes, int n, int ncy, int ncx, int bins,
                       const int32_t *row_idx, int noy, const int32_t *col_idx, int nox, int cells_x,
-                      int cells_y, double eps_term, int32_t *sq, double *norms, cudaStream_t st);
+                      int cells_y, int k, double eps_term, int32_t *sq, double *norms, cudaStream_t st);
 void launch_window_features(const int32_t *grid, int n, int ncy, int ncx, int bins,
                             const int32_t *row_idx, int noy, const int32_t *col_idx, int nox,
                             int cells_x, int cells_y, int block, int bstride, int norm,

@@ -104,6 +104,34 @@ __global__ void k_window_l2(const int32_t *__restrict__ sq, int n, int ncy, int 
     norms[i] = __dsqrt_rn(__dadd_rn((double)s, eps_term));
 }
 
+// Regular lattice (window (iy, ix) reads cells (iy + cy*K, ix + cx*K)): the
+// window sum is separable, so pass 2 sums cells_x cells along each lattice row
+// into hs, and pass 3 sums cells_y of those down each window column.
+__global__ void k_window_l2_h(const int32_t *__restrict__ sq, int64_t rows_total, int ncx, int nox,
+                              int cells_x, int K, int32_t *__restrict__ hs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows_total * nox) return;
+    const int ix = (int)(i % nox);
+    const int64_t r = i / nox;  // (frame, lattice row)
+    const int32_t *row = sq + r * ncx + ix;
+    int32_t s = 0;
+    for (int cx = 0; cx < cells_x; ++cx) s += __ldg(row + cx * K);
+    hs[i] = s;
+}
+
+__global__ void k_window_l2_v(const int32_t *__restrict__ hs, int n, int ncy, int noy, int nox,
+                              int cells_y, int K, double eps_term, double *__restrict__ norms) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)n * noy * nox) return;
+    const int ix = (int)(i % nox);
+    const int64_t r = i / nox;
+    const int iy = (int)(r % noy), f = (int)(r / noy);
+    const int32_t *col = hs + ((int64_t)f * ncy + iy) * nox + ix;
+    int64_t s = 0;
+    for (int cy = 0; cy < cells_y; ++cy) s += __ldg(col + (int64_t)cy * K * nox);
+    norms[i] = __dsqrt_rn(__dadd_rn((double)s, eps_term));
+}
+
 // ---------------------------------------------------------------------------
 // Window scores on a regular cell lattice (detector.py:140-154 with block = 1,
 // descriptor.py:107-124): the window at lattice origin (iy, ix) reads cells
@@ -350,13 +378,21 @@ void launch_cell_grid(const int32_t *pl, int64_t pp, int64_t pns, int64_t pfs, i
 
 void launch_window_l2(const void *grid, int elem_bytes, int n, int ncy, int ncx, int bins,
                       const int32_t *row_idx, int noy, const int32_t *col_idx, int nox, int cells_x,
-                      int cells_y, double eps_term, int32_t *sq, double *norms, cudaStream_t st) {
+                      int cells_y, int k, double eps_term, int32_t *sq, double *norms, cudaStream_t st) {
     const int64_t cells = (int64_t)n * ncy * ncx;
     if (elem_bytes == 1)
         k_cell_sq<uint8_t><<<blocks_for(cells, 256), 256, 0, st>>>((const uint8_t *)grid, cells, bins, sq);
     else
         k_cell_sq<int32_t><<<blocks_for(cells, 256), 256, 0, st>>>((const int32_t *)grid, cells, bins, sq);
     const int64_t tot = (int64_t)n * noy * nox;
+    if (k > 0) {  // regular lattice: separable sums (hs reuses the tail of sq's buffer? no: own area)
+        int32_t *hs = sq + cells;
+        k_window_l2_h<<<blocks_for((int64_t)n * ncy * nox, 256), 256, 0, st>>>(sq, (int64_t)n * ncy, ncx,
+                                                                              nox, cells_x, k, hs);
+        k_window_l2_v<<<blocks_for(tot, 256), 256, 0, st>>>(hs, n, ncy, noy, nox, cells_y, k, eps_term,
+                                                             norms);
+        return;
+    }
     k_window_l2<<<blocks_for(tot, 128), 128, 0, st>>>(sq, n, ncy, ncx, row_idx, noy, col_idx, nox,
                                                       cells_x, cells_y, eps_term, norms);
 }

@@ -146,7 +146,9 @@ class HogPipeline:
         self.window_norms = None
         if window_norm is not None:
             self.window_norms = t.empty((n, len(self.oys), len(self.oxs)), dtype=t.float64, device=dev)
-            self.cell_sq = t.empty((n, self.ncy, self.ncx), dtype=t.int32, device=dev)
+            # per-cell sums of squares, then (regular lattice) per-row window sums
+            self.cell_sq = t.empty(n * self.ncy * (self.ncx + len(self.oxs)), dtype=t.int32,
+                                   device=dev)
         self.band_rows_timings = None
         if band_rows is None and self.chunks == 1 and _tune_enabled():
             self.band_rows = self._tune_band_rows()
@@ -392,9 +394,10 @@ class HogPipeline:
         if self.window_norms is not None:
             _native.call("hog_window_l2", gp, self.grid.element_size(), n, self.ncy, self.ncx,
                          self.bins, D.ptr(self.ri_dev), len(self.oys), D.ptr(self.ci_dev),
-                         len(self.oxs), g.cells_x, g.cells_y, eps_term("l2"),
-                         D.ptr(self.cell_sq) + 4 * a * cells, D.ptr(self.window_norms) + 8 * a * nwin,
-                         s)
+                         len(self.oxs), g.cells_x, g.cells_y,
+                         self.cell // self.stride if self.fused else 0, eps_term("l2"),
+                         D.ptr(self.cell_sq) + 4 * a * self.ncy * (self.ncx + len(self.oxs)),
+                         D.ptr(self.window_norms) + 8 * a * nwin, s)
         if self.scores is not None and self.fused and g.cells_x == 8 and self.grid_u8:
             _native.call("hog_scores_lattice_u8", gp, n, self.ncy, self.ncx,
                          self.bins, len(self.oys), len(self.oxs), g.cells_x, g.cells_y,

@@ -45,7 +45,8 @@ class HostGather:
     pinned-buffer copy.  `rows` is this rank's range of the leading axis.
     """
 
-    def __init__(self, tag: str, shape, dtype, rows: range, rank: int, barrier, pin: bool = True):
+    def __init__(self, tag: str, shape, dtype, rows: range, rank: int, barrier, pin: bool = True,
+                 single_process: bool = False):
         import mmap
         import os
 
@@ -55,16 +56,21 @@ class HostGather:
         self.shape, self.dtype = tuple(int(s) for s in shape), np.dtype(dtype)
         self.nbytes = int(np.prod(self.shape, dtype=np.int64)) * self.dtype.itemsize
         self.path = f"/dev/shm/hogb200_{tag}"
-        if rank == 0:
+        if single_process:
+            self.path = None  # one process: a private page-locked mapping is the same gather
+        if rank == 0 and self.path:
             with open(self.path, "wb") as f:
                 f.truncate(max(self.nbytes, 1))
         barrier()
-        fd = os.open(self.path, os.O_RDWR)
-        try:
-            self._mm = mmap.mmap(fd, max(self.nbytes, 1), mmap.MAP_SHARED,
-                                 mmap.PROT_READ | mmap.PROT_WRITE)
-        finally:
-            os.close(fd)
+        if self.path:
+            fd = os.open(self.path, os.O_RDWR)
+            try:
+                self._mm = mmap.mmap(fd, max(self.nbytes, 1), mmap.MAP_SHARED,
+                                     mmap.PROT_READ | mmap.PROT_WRITE)
+            finally:
+                os.close(fd)
+        else:
+            self._mm = mmap.mmap(-1, max(self.nbytes, 1))
         self.array = np.frombuffer(self._mm, dtype=self.dtype,
                                    count=int(np.prod(self.shape, dtype=np.int64))).reshape(self.shape)
         self.rows = rows
@@ -102,7 +108,7 @@ class HostGather:
         except BufferError:  # views still held by the caller: unmapped when they go
             pass
         self._barrier()
-        if self.rank == 0:
+        if self.rank == 0 and self.path:
             try:
                 os.unlink(self.path)
             except FileNotFoundError:
