@@ -60,6 +60,20 @@ const char *hog_version(void);
 /* Text of the last error raised on the calling thread ("" if none). */
 const char *hog_last_error(void);
 
+/* Octant binning (N_b in {4, 8}).  gradient.py:55-72: the reference's
+ * table for these bin counts is folded by its quarter/half-turn symmetry into
+ * sign tests of four linear forms evaluated in registers (no table gather).
+ * hog_lut_proof runs that device classifier on all 261,121 (dx, dy) pairs and
+ * stores in *mismatches the entries where it differs from `lut` (0: proven
+ * identical; -1: bins not 4 or 8).  It synchronises `stream`.  hog_grad_bin /
+ * hog_pipeline use the octant kernel only for a (device, lut, bins) that has
+ * passed this proof (run automatically on first use outside a graph capture;
+ * otherwise the table-gather kernel runs).  Tables are treated as immutable,
+ * like the reference's read-only OrientationLut: hog_lut_forget drops the
+ * cached result for a table whose bytes the caller rewrites. */
+int hog_lut_proof(const uint8_t *lut, int bins, long long *mismatches, hog_stream_t stream);
+void hog_lut_forget(const uint8_t *lut);
+
 /* Fast-path plane row pitch (elements) for width w: round_up(w, 8) + 8. */
 int64_t hog_plane_pitch(int w);
 

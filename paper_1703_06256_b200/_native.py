@@ -22,6 +22,8 @@ SIGNATURES = {
     "hog_version": (ctypes.c_char_p, []),
     "hog_last_error": (ctypes.c_char_p, []),
     "hog_plane_pitch": (_L, [_I]),
+    "hog_lut_proof": (_I, [_P, _I, _P, _P]),
+    "hog_lut_forget": (None, [_P]),
     "hog_grad_bin": (_I, [_P, _I, _I, _I, _I, _L, _L, _L, _P, _I, _P, _L, _L, _P]),
     "hog_scratch_bytes": (_SZ, [_I, _I, _I, _I, _I, _I]),
     "hog_set_band_rows": (None, [_I]),

@@ -21,6 +21,9 @@
 //   column) while it bins the image, and k_scan_cols turns those counts into
 //   the column counts above every band.  When the scan lattice is regular,
 //   k_planes also emits the cell-histogram grid from the plane values it
+#include <map>
+#include <mutex>
+
 #include "hog_common.cuh"
 
 namespace hogb200 {
@@ -48,6 +51,58 @@ int check_launch(const char *what) {
 static int env_int(const char *name, int dflt) {
     const char *e = getenv(name);
     return (e && *e) ? atoi(e) : dflt;
+}
+
+// Tables proven equal to the octant classifier (k_lut_proof), per device.
+// A table handed to the library is treated as immutable, like the
+// reference's read-only OrientationLut (gradient.py:55-72); hog_lut_forget
+// drops a pointer whose contents the caller rewrites.
+struct LutKey {
+    int dev;
+    const uint8_t *lut;
+    int bins;
+    bool operator<(const LutKey &o) const {
+        return dev != o.dev ? dev < o.dev : lut != o.lut ? lut < o.lut : bins < o.bins;
+    }
+};
+static std::mutex g_lut_mu;
+static std::map<LutKey, bool> g_lut_ok;
+
+// mismatching (dx, dy) entries of the table against the octant classifier
+// (-1: bins not handled by it; -2: CUDA error)
+static long long lut_proof_run(const uint8_t *lut, int bins, cudaStream_t st) {
+    if (bins != 4 && bins != 8) return -1;
+    unsigned long long *d = nullptr, h = 0;
+    if (cudaMallocAsync(&d, sizeof(h), st) != cudaSuccess) return -2;
+    cudaMemsetAsync(d, 0, sizeof(h), st);
+    launch_lut_proof(bins, lut, d, st);
+    cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(d, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return -2;
+    return (long long)h;
+}
+
+bool lut_proven(const uint8_t *lut, int bins, cudaStream_t st) {
+    if (bins != 4 && bins != 8) return false;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    const LutKey key{dev, lut, bins};
+    {
+        std::lock_guard<std::mutex> lk(g_lut_mu);
+        auto it = g_lut_ok.find(key);
+        if (it != g_lut_ok.end()) return it->second;
+    }
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+        return false;  // cannot synchronise inside a capture: the table-gather kernel runs
+    const long long bad = lut_proof_run(lut, bins, st);
+    if (bad < -1) {
+        cudaGetLastError();
+        return false;
+    }
+    std::lock_guard<std::mutex> lk(g_lut_mu);
+    g_lut_ok[key] = bad == 0;
+    return bad == 0;
 }
 
 // Band rows R of the plane kernel for this thread's next calls (0: automatic).
@@ -126,7 +181,9 @@ TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int ce
         g.S1 = s_env;
     } else if (s_env <= 0) {
         const int64_t target = (int64_t)4 * 148 * 64;  // warps: ~4 full waves
-        while (R % (2 * g.S1) == 0 && R / (2 * g.S1) >= 16 &&
+        // octant binning (N_b 4 / 8) counts in blocks of 8 rows: keep R1 % 8 == 0
+        const bool oct = bins == 4 || bins == 8;
+        while (R % (2 * g.S1) == 0 && R / (2 * g.S1) >= 16 && (!oct || (R / (2 * g.S1)) % 8 == 0) &&
                (int64_t)n * ((h + R / g.S1 - 1) / (R / g.S1)) * ((w + CHUNK - 1) / CHUNK) < target)
             g.S1 *= 2;
     }
@@ -285,6 +342,26 @@ extern "C" {
 const char *hog_version(void) { return "hogb200 1.2 sm_100a"; }
 
 const char *hog_last_error(void) { return g_err.c_str(); }
+
+int hog_lut_proof(const uint8_t *lut, int bins, long long *mismatches, hog_stream_t stream) {
+    g_err.clear();
+    if (!lut || !mismatches) return fail(HOG_EINVAL, "null pointer");
+    const long long bad = lut_proof_run(lut, bins, (cudaStream_t)stream);
+    if (bad < -1) return check_launch("hog_lut_proof") ? HOG_ECUDA : fail(HOG_ECUDA, "hog_lut_proof failed");
+    *mismatches = bad;
+    int dev = 0;
+    if (bad >= 0 && cudaGetDevice(&dev) == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(g_lut_mu);
+        g_lut_ok[LutKey{dev, lut, bins}] = bad == 0;
+    }
+    return HOG_OK;
+}
+
+void hog_lut_forget(const uint8_t *lut) {
+    std::lock_guard<std::mutex> lk(g_lut_mu);
+    for (auto it = g_lut_ok.begin(); it != g_lut_ok.end();)
+        it = it->first.lut == lut ? g_lut_ok.erase(it) : std::next(it);
+}
 
 int64_t hog_plane_pitch(int w) { return round_up((int64_t)w, 8) + 8; }
 

@@ -256,6 +256,11 @@ __global__ void k_scan_cols(TileGeom g, Scratch sc) {
     for (; nextb < g.nb2; ++nextb) store_v(nextb);  // bands starting at or past the last row
 }
 
+static bool oct_enabled() {
+    const char *e = getenv("HOGB200_OCTANT");  // 0: always the table-gather kernel (A/B)
+    return !(e && *e && atoi(e) == 0);
+}
+
 template <int NWB>
 void grad_bin_t(int c, bool counts, const uint8_t *img, int64_t ip, int64_t ics, int64_t ifs,
                 const uint8_t *lut, int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g,
@@ -276,6 +281,15 @@ void grad_bin_t(int c, bool counts, const uint8_t *img, int64_t ip, int64_t ics,
 void launch_grad_bin(int nwb, int c, bool counts, const uint8_t *img, int64_t ip, int64_t ics,
                      int64_t ifs, const uint8_t *lut, int8_t *bm, int64_t bp, int64_t bfs,
                      const TileGeom &g, const Scratch &sc, cudaStream_t st) {
+    // N_b in {4, 8} with the reference's table: the octant kernel (no table
+    // gather; k_bin_oct.cu).  It reads and writes 8-byte row groups, so rows
+    // must be 8-aligned with pitches covering round_up(w, 8).
+    const int64_t w8 = round_up(g.w, 8);
+    const bool a8 = ((uintptr_t)img & 7) == 0 && ((uintptr_t)bm & 7) == 0 && ip % 8 == 0 &&
+                    ifs % 8 == 0 && bp % 8 == 0 && bfs % 8 == 0 && ip >= w8 && bp >= w8;
+    if (c == 1 && (g.bins == 4 || g.bins == 8) && a8 && oct_enabled() && lut_proven(lut, g.bins, st) &&
+        launch_grad_bin_oct(g.bins, counts, img, ip, ifs, bm, bp, bfs, g, sc, st))
+        return;
     switch (nwb) {
         case 1: grad_bin_t<1>(c, counts, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st); break;
         case 2: grad_bin_t<2>(c, counts, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st); break;
