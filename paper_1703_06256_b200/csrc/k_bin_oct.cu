@@ -167,9 +167,18 @@ __device__ __forceinline__ void unslice(const Slice &s, uint32_t (&lo)[4], uint3
 
 }  // namespace
 
+// rows of loads in flight ahead of the row being binned (B200 A/B: tools/ab_r2.sh)
+#ifndef K1_OCT_PF
+#define K1_OCT_PF 2
+#endif
+
 // counts as in k_grad_bin (C[f][b][x][w], u8x4 of bins 4w..4w+3) when COUNTS
+#ifndef K1_OCT_MINB
+#define K1_OCT_MINB 1
+#endif
+
 template <int NB, bool COUNTS>
-__global__ void __launch_bounds__(K_THREADS)
+__global__ void __launch_bounds__(K_THREADS, K1_OCT_MINB)
 k_grad_bin_oct(const uint8_t *__restrict__ img, int64_t ip, int64_t ifs, int8_t *__restrict__ bm,
                int64_t bp, int64_t bfs, TileGeom g, Scratch sc) {
     const int lane = threadIdx.x & 31, seg = lane >> 4, sl = lane & 15;
@@ -212,17 +221,29 @@ k_grad_bin_oct(const uint8_t *__restrict__ img, int64_t ip, int64_t ifs, int8_t 
         nvc[k] = v;
     }
 
-    uint2 wa, wc, wb;  // rows y-1, y, y+1
+    // rows y-1, y, y+1 as fp16x2 pairs; rows y+2 .. y+K1_OCT_PF raw (loads in flight)
+    uint2 qw[K1_OCT_PF];
+    uint32_t ql[K1_OCT_PF], qr[K1_OCT_PF];
     uint32_t elc = 0, erc = 0, elb = 0, erb = 0;
+    Row8 ra, rc, rb;
     {
         const uint8_t *pa = rowp(y0 - 1), *pc = rowp(y0), *pb = rowp(y0 + 1);
-        wa = __ldg(reinterpret_cast<const uint2 *>(pa));
-        wc = __ldg(reinterpret_cast<const uint2 *>(pc));
-        wb = __ldg(reinterpret_cast<const uint2 *>(pb));
+        const uint2 wa = __ldg(reinterpret_cast<const uint2 *>(pa));
+        const uint2 wc = __ldg(reinterpret_cast<const uint2 *>(pc));
+        const uint2 wb = __ldg(reinterpret_cast<const uint2 *>(pb));
         if (has_l) elc = __ldg(pc - 1), elb = __ldg(pb - 1);
         if (has_r) erc = __ldg(pc + 8), erb = __ldg(pb + 8);
+#pragma unroll
+        for (int i = 0; i + 1 < K1_OCT_PF; ++i) {
+            const uint8_t *pq = rowp(y0 + 2 + i);
+            qw[i] = __ldg(reinterpret_cast<const uint2 *>(pq));
+            ql[i] = has_l ? __ldg(pq - 1) : 0u;
+            qr[i] = has_r ? __ldg(pq + 8) : 0u;
+        }
+        ra = spread(wa.x, wa.y);
+        rc = spread(wc.x, wc.y);
+        rb = spread(wb.x, wb.y);
     }
-    Row8 ra = spread(wa.x, wa.y), rc = spread(wc.x, wc.y), rb = spread(wb.x, wb.y);
     int8_t *bout = bm + (int64_t)f * bfs + (int64_t)y0 * bp + x;
     // rows whose pixels get bins: [rlo, rhi) (frame border rows are NO_BIN unless
     // the slab continues past them); dead half-warps bin nothing
@@ -234,7 +255,7 @@ k_grad_bin_oct(const uint8_t *__restrict__ img, int64_t ip, int64_t ifs, int8_t 
     const uint32_t nstore = (live && x < g.w) ? (uint32_t)(y1 - y0) : 0u;
     // last readable row: the row pointer stops there
     const int64_t pmax = (int64_t)(g.h - 1 + g.hb) * ip;
-    int64_t poff = (int64_t)min(max(y0 + 2, -g.ht), g.h - 1 + g.hb) * ip;
+    int64_t poff = (int64_t)min(max(y0 + 1 + K1_OCT_PF, -g.ht), g.h - 1 + g.hb) * ip;
     const uint8_t *colf = col;
     const uint32_t Lsel = sl == 0 ? 0xffffffffu : 0u, Rsel = sl == 15 ? 0xffffffffu : 0u;
 
@@ -249,7 +270,7 @@ k_grad_bin_oct(const uint8_t *__restrict__ img, int64_t ip, int64_t ifs, int8_t 
 
     // one row: classify, store, return the two one-hot words
     auto row = [&](int y, uint32_t (&oh)[2]) {
-        // row y+2 in flight while row y is binned
+        // row y+1+K1_OCT_PF in flight while row y is binned
         const uint8_t *pd = colf + poff;
         const uint2 wd = __ldg(reinterpret_cast<const uint2 *>(pd));
         uint32_t eld = 0, erd = 0;
@@ -280,9 +301,12 @@ k_grad_bin_oct(const uint8_t *__restrict__ img, int64_t ip, int64_t ifs, int8_t 
         bout += bp;
         ra = rc;
         rc = rb;
-        rb = spread(wd.x, wd.y);
         elc = elb, erc = erb;
-        elb = eld, erb = erd;
+        qw[K1_OCT_PF - 1] = wd, ql[K1_OCT_PF - 1] = eld, qr[K1_OCT_PF - 1] = erd;
+        rb = spread(qw[0].x, qw[0].y);
+        elb = ql[0], erb = qr[0];
+#pragma unroll
+        for (int i = 0; i + 1 < K1_OCT_PF; ++i) qw[i] = qw[i + 1], ql[i] = ql[i + 1], qr[i] = qr[i + 1];
     };
 
     int y = y0;
