@@ -173,8 +173,11 @@ __device__ __forceinline__ void unslice(const Slice &s, uint32_t (&lo)[4], uint3
 #endif
 
 // counts as in k_grad_bin (C[f][b][x][w], u8x4 of bins 4w..4w+3) when COUNTS
+#ifndef K1_OCT_ROLL
+#define K1_OCT_ROLL 0
+#endif
 #ifndef K1_OCT_MINB
-#define K1_OCT_MINB 1
+#define K1_OCT_MINB 4
 #endif
 
 template <int NB, bool COUNTS>
@@ -310,6 +313,44 @@ k_grad_bin_oct(const uint8_t *__restrict__ img, int64_t ip, int64_t ifs, int8_t 
     };
 
     int y = y0;
+#if K1_OCT_ROLL
+    // row pairs in a rolled loop; the carry-save tree advances by a uniform
+    // pair counter (fewer live registers than the unrolled 8-row block)
+    uint32_t t2a[2] = {0, 0}, t4a[2] = {0, 0};
+    const int npairs = ((iters + 7) >> 3) << 2;
+#pragma unroll 1
+    for (int pr = 0; pr < npairs; ++pr) {
+        uint32_t oa[2], ob[2];
+        row(y, oa);
+        row(y + 1, ob);
+        y += 2;
+        if (COUNTS) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                uint32_t c2;
+                csa(ones[k], c2, ones[k], oa[k], ob[k]);
+                if ((pr & 1) == 0) {
+                    t2a[k] = c2;
+                } else {
+                    uint32_t c4;
+                    csa(twos[k], c4, twos[k], t2a[k], c2);
+                    if ((pr & 2) == 0) {
+                        t4a[k] = c4;
+                    } else {
+                        uint32_t c;
+                        csa(fours[k], c, fours[k], t4a[k], c4);
+#pragma unroll
+                        for (int j = 3; j < 8; ++j) {
+                            const uint32_t q = S[k].q[j];
+                            S[k].q[j] = q ^ c;
+                            c &= q;
+                        }
+                    }
+                }
+            }
+        }
+    }
+#else
     for (int it = 0; it < iters; it += 8) {
         // 8 rows: carry-save tree ones/twos/fours, one eights carry rippled into q[3..7]
         uint32_t e8[2];
@@ -348,6 +389,7 @@ k_grad_bin_oct(const uint8_t *__restrict__ img, int64_t ip, int64_t ifs, int8_t 
             }
         }
     }
+#endif
     if (COUNTS && live) {  // columns past w get zero counts (k_scan_cols reads them)
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
