@@ -251,6 +251,26 @@ int check_bins(int bins) {
     return HOG_OK;
 }
 
+// Sub-bands of the octant binning kernel (gray, N_b 4 / 8).  It runs whole
+// bands per half-warp where the batch fills the GPU -- its per-unit setup and
+// count transposes then amortise over R rows (B200, c2: 0.155 ms with R/4-row
+// sub-bands, 0.140 ms with R-row ones) -- and splits bands (R1 a multiple of
+// 8) only until the grid is ~2 waves of its 4 CTAs per SM (64-frame shards,
+// single frames).  smax: the sub-band count the scratch was sized for.
+static void oct_subbands(TileGeom &g, int c, int smax) {
+    if (c != 1 || (g.bins != 4 && g.bins != 8) || env_int("HOGB200_SUBBANDS", 0) > 0) return;
+    auto ctas = [&](int s) {
+        const int r1 = g.R / s;
+        return (int64_t)g.n * ((g.h + r1 - 1) / r1) * g.nc1 / 8;  // 8 half-warp units per CTA
+    };
+    int s = 1;
+    while (2 * s <= smax && g.R % (2 * s) == 0 && (g.R / (2 * s)) % 8 == 0 && ctas(s) < 2 * 148 * 4)
+        s *= 2;
+    g.S1 = s;
+    g.R1 = g.R / s;
+    g.nb1 = (g.h + g.R1 - 1) / g.R1;
+}
+
 int check_pitch4(const void *p, int64_t pitch, int w, const char *what) {
     if (((uintptr_t)p & 3) != 0 || pitch % 4 != 0 || pitch < round_up(w, 4))
         return fail(HOG_EINVAL, "%s: need 4-byte aligned base and pitch %% 4 == 0, pitch >= %lld (got %lld)",
@@ -375,11 +395,7 @@ int hog_grad_bin(const uint8_t *img, int n, int c, int h, int w, int64_t ip, int
     if ((e = check_pitch4(img, ip, w, "image")) || (e = check_pitch4(bm, bp, w, "binmap"))) return e;
     if (!img || !lut || !bm) return fail(HOG_EINVAL, "null buffer");
     TileGeom g = make_geom(n, h, w, bins, false, 0, 0, false, false);
-    if (c == 1 && (bins == 4 || bins == 8) && env_int("HOGB200_SUBBANDS", 0) <= 0) {
-        g.S1 = 1;  // octant binning: whole bands per half-warp (see pipeline_impl)
-        g.R1 = g.R;
-        g.nb1 = (h + g.R - 1) / g.R;
-    }
+    oct_subbands(g, c, 1 << 20);  // no counts: no scratch bound on the sub-bands
     Scratch sc{};
     launch_grad_bin(1, c, false, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, (cudaStream_t)stream);
     return check_launch("hog_grad_bin");
@@ -464,15 +480,7 @@ static int pipeline_impl(const uint8_t *img, int n, int c, int h, int w, int64_t
                            po.vec != 0 && !want_fused);
     g.ht = halo_top ? 1 : 0;
     g.hb = halo_bot ? 1 : 0;
-    // Octant binning (gray, N_b 4 / 8): one whole band of R rows per half-warp,
-    // so its per-unit setup and count transposes amortise over R rows (B200,
-    // c2: 0.155 ms with R/4-row sub-bands, 0.140 ms with R-row ones); the
-    // scratch sized for the sub-banded geometry covers it (fewer sub-bands).
-    if (c == 1 && (bins == 4 || bins == 8) && env_int("HOGB200_SUBBANDS", 0) <= 0) {
-        g.S1 = 1;
-        g.R1 = g.R;
-        g.nb1 = (h + g.R - 1) / g.R;
-    }
+    oct_subbands(g, c, g.S1);  // never more sub-bands than the scratch was sized for
     Scratch sc{};
     size_t need = carve(g, nullptr, nullptr);
     if (scratch == nullptr || sbytes < need)
