@@ -103,6 +103,9 @@ struct GridOut {
 };
 
 constexpr int K2_G = 4;  // rows per phase-A/phase-B group
+#ifndef K2_FASTGROUP
+#define K2_FASTGROUP 1  // guard-free code path for full row groups (k_planes.cuh)
+#endif
 
 // Max threads per k_planes CTA (NWARP compute warps [+ the TMA store warp]),
 // i.e. the register budget at two CTAs per SM: 256 threads -> 128 registers,
