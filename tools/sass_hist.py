@@ -16,7 +16,9 @@ KERNELS = [
      r"k_planesILi4ELi2ELi4ELb1ELi0ELb0ELb1EE"),
     ("k_planes c4 (NW=4, lattice step 8, 8 cols/lane)", r"k_planesILi4ELi1ELi8ELb1ELi0ELb0ELb0EE"),
     ("k_planes c5 (NW=9, 18 bins, lattice step 8)", r"k_planesILi9ELi1ELi4ELb1ELi0ELb0ELb0EE"),
-    ("k_grad_bin gray, 8 bins, counts", r"k_grad_binILi1ELi2ELb1EE"),
+    ("k_grad_bin_oct gray, 8 bins, counts (c1/c2: fp16x2 octant sign tests, no table gather)",
+     r"k_grad_bin_octILi8ELb1EE"),
+    ("k_grad_bin gray, 8 bins, counts (table gather: any other table)", r"k_grad_binILi1ELi2ELb1EE"),
     ("k_grad_bin RGB, 8 bins, counts", r"k_grad_binILi3ELi2ELb1EE"),
     ("k_scores_rows, byte grid, 8 bins (c1/c4)", r"k_scores_rowsILi1ELi\d+ELi8ELb1ELi4EE"),
     ("k_scores_rows, byte grid, 18 bins (c5)", r"k_scores_rowsILi1ELi\d+ELi18ELb1ELi4EE"),
