@@ -258,7 +258,7 @@ int check_bins(int bins) {
 // 8) only until the grid is ~2 waves of its 4 CTAs per SM (64-frame shards,
 // single frames).  smax: the sub-band count the scratch was sized for.
 static void oct_subbands(TileGeom &g, int c, int smax) {
-    if (c != 1 || (g.bins != 4 && g.bins != 8) || env_int("HOGB200_SUBBANDS", 0) > 0) return;
+    if ((c != 1 && c != 3) || (g.bins != 4 && g.bins != 8) || env_int("HOGB200_SUBBANDS", 0) > 0) return;
     auto ctas = [&](int s) {
         const int r1 = g.R / s;
         return (int64_t)g.n * ((g.h + r1 - 1) / r1) * g.nc1 / 8;  // 8 half-warp units per CTA

@@ -307,9 +307,9 @@ void launch_grad_bin(int nwb, int c, bool counts, const uint8_t *img, int64_t ip
                      int64_t ifs, const uint8_t *lut, int8_t *bm, int64_t bp, int64_t bfs,
                      const TileGeom &g, const Scratch &sc, cudaStream_t st);
 // k_bin_oct.cu: table-free binning for N_b in {4, 8} (false: bins not handled)
-bool launch_grad_bin_oct(int bins, bool counts, const uint8_t *img, int64_t ip, int64_t ifs,
-                         int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g, const Scratch &sc,
-                         cudaStream_t st);
+bool launch_grad_bin_oct(int bins, int c, bool counts, const uint8_t *img, int64_t ip, int64_t ics,
+                         int64_t ifs, int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g,
+                         const Scratch &sc, cudaStream_t st);
 bool launch_lut_proof(int bins, const uint8_t *lut, unsigned long long *mismatches, cudaStream_t st);
 // hog_abi.cu: has this (device, table, bins) passed k_lut_proof?  Proves it on
 // first use (synchronising st) unless st is capturing a graph.

@@ -256,9 +256,12 @@ __global__ void k_scan_cols(TileGeom g, Scratch sc) {
     for (; nextb < g.nb2; ++nextb) store_v(nextb);  // bands starting at or past the last row
 }
 
-static bool oct_enabled() {
-    const char *e = getenv("HOGB200_OCTANT");  // 0: always the table-gather kernel (A/B)
-    return !(e && *e && atoi(e) == 0);
+// HOGB200_OCTANT: 0 = always the table-gather kernel; 1 = octant for gray
+// only; default: gray and RGB (A/B switches)
+static bool oct_enabled(int c) {
+    const char *e = getenv("HOGB200_OCTANT");
+    const int v = (e && *e) ? atoi(e) : 2;
+    return v >= 2 || (v == 1 && c == 1);
 }
 
 template <int NWB>
@@ -286,9 +289,11 @@ void launch_grad_bin(int nwb, int c, bool counts, const uint8_t *img, int64_t ip
     // must be 8-aligned with pitches covering round_up(w, 8).
     const int64_t w8 = round_up(g.w, 8);
     const bool a8 = ((uintptr_t)img & 7) == 0 && ((uintptr_t)bm & 7) == 0 && ip % 8 == 0 &&
-                    ifs % 8 == 0 && bp % 8 == 0 && bfs % 8 == 0 && ip >= w8 && bp >= w8;
-    if (c == 1 && (g.bins == 4 || g.bins == 8) && a8 && oct_enabled() && lut_proven(lut, g.bins, st) &&
-        launch_grad_bin_oct(g.bins, counts, img, ip, ifs, bm, bp, bfs, g, sc, st))
+                    ifs % 8 == 0 && (c == 1 || ics % 8 == 0) && bp % 8 == 0 && bfs % 8 == 0 &&
+                    ip >= w8 && bp >= w8;
+    if ((c == 1 || c == 3) && (g.bins == 4 || g.bins == 8) && a8 && oct_enabled(c) &&
+        lut_proven(lut, g.bins, st) &&
+        launch_grad_bin_oct(g.bins, c, counts, img, ip, ics, ifs, bm, bp, bfs, g, sc, st))
         return;
     switch (nwb) {
         case 1: grad_bin_t<1>(c, counts, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st); break;

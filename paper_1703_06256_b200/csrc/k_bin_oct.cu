@@ -65,6 +65,16 @@ __device__ __forceinline__ uint32_t heq0_mask(uint32_t a) {
     return r;
 }
 
+// dx^2 + dy^2 of both halves of a pair, exact in fp32 (<= 130,050): FHFMA
+// (fp16 operands, fp32 accumulate) reads the halves in place
+__device__ __forceinline__ void mag2(uint32_t dx, uint32_t dy, float &lo, float &hi) {
+    asm("{ .reg .f16 xl, xh, yl, yh; .reg .f32 t, u;\n"
+        "  mov.b32 {xl, xh}, %2; mov.b32 {yl, yh}, %3;\n"
+        "  fma.rn.f32.f16 t, yl, yl, 0f00000000; fma.rn.f32.f16 %0, xl, xl, t;\n"
+        "  fma.rn.f32.f16 u, yh, yh, 0f00000000; fma.rn.f32.f16 %1, xh, xh, u; }"
+        : "=f"(lo), "=f"(hi) : "r"(dx), "r"(dy));
+}
+
 constexpr uint32_t H1024 = 0x64646464u;  // byte b -> half 1024 + b (with the 0x64 high byte)
 constexpr uint32_t P512 = 0x60006000u;   // half2(512, 512)
 constexpr uint32_t M512 = 0xE000E000u;   // half2(-512, -512)
@@ -180,10 +190,17 @@ __device__ __forceinline__ void unslice(const Slice &s, uint32_t (&lo)[4], uint3
 #define K1_OCT_MINB 4
 #endif
 
-template <int NB, bool COUNTS>
-__global__ void __launch_bounds__(K_THREADS, K1_OCT_MINB)
-k_grad_bin_oct(const uint8_t *__restrict__ img, int64_t ip, int64_t ifs, int8_t *__restrict__ bm,
-               int64_t bp, int64_t bfs, TileGeom g, Scratch sc) {
+#ifndef K1_OCT_MINB3
+#define K1_OCT_MINB3 3
+#endif
+
+// CH = 3: per-channel gradients, the reference's channel rule (largest
+// dx^2 + dy^2, first channel on ties; gradient.py:113-117) on exact fp32
+// magnitudes, then the same octant sign tests on the winning pair
+template <int NB, bool COUNTS, int CH>
+__global__ void __launch_bounds__(K_THREADS, CH == 1 ? K1_OCT_MINB : K1_OCT_MINB3)
+k_grad_bin_oct(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs,
+               int8_t *__restrict__ bm, int64_t bp, int64_t bfs, TileGeom g, Scratch sc) {
     const int lane = threadIdx.x & 31, seg = lane >> 4, sl = lane & 15;
     const int64_t nunits = (int64_t)g.n * g.nb1 * g.nc1;
     const int64_t unit0 = 2 * warp_id() + seg;
@@ -225,27 +242,30 @@ k_grad_bin_oct(const uint8_t *__restrict__ img, int64_t ip, int64_t ifs, int8_t 
     }
 
     // rows y-1, y, y+1 as fp16x2 pairs; rows y+2 .. y+K1_OCT_PF raw (loads in flight)
-    uint2 qw[K1_OCT_PF];
-    uint32_t ql[K1_OCT_PF], qr[K1_OCT_PF];
-    uint32_t elc = 0, erc = 0, elb = 0, erb = 0;
-    Row8 ra, rc, rb;
-    {
-        const uint8_t *pa = rowp(y0 - 1), *pc = rowp(y0), *pb = rowp(y0 + 1);
+    uint2 qw[CH][K1_OCT_PF];
+    uint32_t ql[CH][K1_OCT_PF], qr[CH][K1_OCT_PF];
+    uint32_t elc[CH], erc[CH], elb[CH], erb[CH];
+    Row8 ra[CH], rc[CH], rb[CH];
+#pragma unroll
+    for (int ch = 0; ch < CH; ++ch) {
+        const uint8_t *pa = rowp(y0 - 1) + ch * ics, *pc = rowp(y0) + ch * ics, *pb = rowp(y0 + 1) + ch * ics;
         const uint2 wa = __ldg(reinterpret_cast<const uint2 *>(pa));
         const uint2 wc = __ldg(reinterpret_cast<const uint2 *>(pc));
         const uint2 wb = __ldg(reinterpret_cast<const uint2 *>(pb));
-        if (has_l) elc = __ldg(pc - 1), elb = __ldg(pb - 1);
-        if (has_r) erc = __ldg(pc + 8), erb = __ldg(pb + 8);
+        elc[ch] = has_l ? __ldg(pc - 1) : 0u;
+        elb[ch] = has_l ? __ldg(pb - 1) : 0u;
+        erc[ch] = has_r ? __ldg(pc + 8) : 0u;
+        erb[ch] = has_r ? __ldg(pb + 8) : 0u;
 #pragma unroll
         for (int i = 0; i + 1 < K1_OCT_PF; ++i) {
-            const uint8_t *pq = rowp(y0 + 2 + i);
-            qw[i] = __ldg(reinterpret_cast<const uint2 *>(pq));
-            ql[i] = has_l ? __ldg(pq - 1) : 0u;
-            qr[i] = has_r ? __ldg(pq + 8) : 0u;
+            const uint8_t *pq = rowp(y0 + 2 + i) + ch * ics;
+            qw[ch][i] = __ldg(reinterpret_cast<const uint2 *>(pq));
+            ql[ch][i] = has_l ? __ldg(pq - 1) : 0u;
+            qr[ch][i] = has_r ? __ldg(pq + 8) : 0u;
         }
-        ra = spread(wa.x, wa.y);
-        rc = spread(wc.x, wc.y);
-        rb = spread(wb.x, wb.y);
+        ra[ch] = spread(wa.x, wa.y);
+        rc[ch] = spread(wc.x, wc.y);
+        rb[ch] = spread(wb.x, wb.y);
     }
     int8_t *bout = bm + (int64_t)f * bfs + (int64_t)y0 * bp + x;
     // rows whose pixels get bins: [rlo, rhi) (frame border rows are NO_BIN unless
@@ -275,26 +295,60 @@ k_grad_bin_oct(const uint8_t *__restrict__ img, int64_t ip, int64_t ifs, int8_t 
     auto row = [&](int y, uint32_t (&oh)[2]) {
         // row y+1+K1_OCT_PF in flight while row y is binned
         const uint8_t *pd = colf + poff;
-        const uint2 wd = __ldg(reinterpret_cast<const uint2 *>(pd));
-        uint32_t eld = 0, erd = 0;
-        if (has_l) eld = __ldg(pd - 1);
-        if (has_r) erd = __ldg(pd + 8);
+        uint2 wd[CH];
+        uint32_t eld[CH], erd[CH];
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+            wd[ch] = __ldg(reinterpret_cast<const uint2 *>(pd + ch * ics));
+            eld[ch] = has_l ? __ldg(pd + ch * ics - 1) : 0u;
+            erd[ch] = has_r ? __ldg(pd + ch * ics + 8) : 0u;
+        }
         poff = min(poff + ip, pmax);
         // halo halves of the centre row: odd byte left of the lane, even byte right of it
-        const uint32_t Oup = __shfl_up_sync(FULL, rc.O1, 1, 16);
-        const uint32_t Edn = __shfl_down_sync(FULL, rc.E0, 1, 16);
-        const uint32_t Oprev = (prmt(elc, H1024, 0x4000) & Lsel) | (Oup & ~Lsel);
-        const uint32_t Enext = (prmt(erc, H1024, 0x0040) & Rsel) | (Edn & ~Rsel);
+        uint32_t Oprev[CH], Enext[CH];
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+            const uint32_t Oup = __shfl_up_sync(FULL, rc[ch].O1, 1, 16);
+            const uint32_t Edn = __shfl_down_sync(FULL, rc[ch].E0, 1, 16);
+            Oprev[ch] = (prmt(elc[ch], H1024, 0x4000) & Lsel) | (Oup & ~Lsel);
+            Enext[ch] = (prmt(erc[ch], H1024, 0x0040) & Rsel) | (Edn & ~Rsel);
+        }
         const bool rowok = (uint32_t)(y - rlo) < nrow_ok;
         uint32_t bins[2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const uint32_t Ec = k ? rc.E1 : rc.E0, Oc = k ? rc.O1 : rc.O0;
-            const uint32_t Op = k ? rc.O0 : Oprev, En = k ? Enext : rc.E1;
-            const uint32_t dxA = hsub2(Oc, prmt(Op, Oc, 0x5432));  // (b1 - b-1, b3 - b1)
-            const uint32_t dxB = hsub2(prmt(Ec, En, 0x5432), Ec);  // (b2 - b0, b4 - b2)
-            const uint32_t dyA = hsub2(k ? rb.E1 : rb.E0, k ? ra.E1 : ra.E0);
-            const uint32_t dyB = hsub2(k ? rb.O1 : rb.O0, k ? ra.O1 : ra.O0);
+            uint32_t dxA, dyA, dxB, dyB;
+            float bmA0 = 0.f, bmA1 = 0.f, bmB0 = 0.f, bmB1 = 0.f;  // winning magnitudes
+#pragma unroll
+            for (int ch = 0; ch < CH; ++ch) {
+                const Row8 &a = ra[ch], &c = rc[ch], &bb = rb[ch];
+                const uint32_t Ec = k ? c.E1 : c.E0, Oc = k ? c.O1 : c.O0;
+                const uint32_t Op = k ? c.O0 : Oprev[ch], En = k ? Enext[ch] : c.E1;
+                const uint32_t xA = hsub2(Oc, prmt(Op, Oc, 0x5432));  // (b1 - b-1, b3 - b1)
+                const uint32_t xB = hsub2(prmt(Ec, En, 0x5432), Ec);  // (b2 - b0, b4 - b2)
+                const uint32_t yA = hsub2(k ? bb.E1 : bb.E0, k ? a.E1 : a.E0);
+                const uint32_t yB = hsub2(k ? bb.O1 : bb.O0, k ? a.O1 : a.O0);
+                if (CH == 1) {
+                    dxA = xA, dyA = yA, dxB = xB, dyB = yB;
+                } else {
+                    float mA0, mA1, mB0, mB1;
+                    mag2(xA, yA, mA0, mA1);
+                    mag2(xB, yB, mB0, mB1);
+                    if (ch == 0) {
+                        dxA = xA, dyA = yA, dxB = xB, dyB = yB;
+                        bmA0 = mA0, bmA1 = mA1, bmB0 = mB0, bmB1 = mB1;
+                    } else {
+                        // lane mask of the halves whose magnitude beats the best so far
+                        // (sign of best - mag; ties keep the earlier channel)
+                        const uint32_t kA = prmt(__float_as_uint(bmA0 - mA0), __float_as_uint(bmA1 - mA1), 0xFFBB);
+                        const uint32_t kB = prmt(__float_as_uint(bmB0 - mB0), __float_as_uint(bmB1 - mB1), 0xFFBB);
+                        dxA = (xA & kA) | (dxA & ~kA), dyA = (yA & kA) | (dyA & ~kA);
+                        dxB = (xB & kB) | (dxB & ~kB), dyB = (yB & kB) | (dyB & ~kB);
+                        bmA0 = fmaxf(bmA0, mA0), bmA1 = fmaxf(bmA1, mA1);
+                        bmB0 = fmaxf(bmB0, mB0), bmB1 = fmaxf(bmB1, mB1);
+                    }
+                }
+            }
             uint32_t m0, m1, m2, mz;
             oct_masks<NB>(dxA, dyA, dxB, dyB, m0, m1, m2, mz);
             const uint32_t nv = (rowok ? nvc[k] : 0xffffffffu) | mz;
@@ -302,14 +356,18 @@ k_grad_bin_oct(const uint8_t *__restrict__ img, int64_t ip, int64_t ifs, int8_t 
         }
         if ((uint32_t)(y - y0) < nstore) *reinterpret_cast<uint2 *>(bout) = make_uint2(bins[0], bins[1]);
         bout += bp;
-        ra = rc;
-        rc = rb;
-        elc = elb, erc = erb;
-        qw[K1_OCT_PF - 1] = wd, ql[K1_OCT_PF - 1] = eld, qr[K1_OCT_PF - 1] = erd;
-        rb = spread(qw[0].x, qw[0].y);
-        elb = ql[0], erb = qr[0];
 #pragma unroll
-        for (int i = 0; i + 1 < K1_OCT_PF; ++i) qw[i] = qw[i + 1], ql[i] = ql[i + 1], qr[i] = qr[i + 1];
+        for (int ch = 0; ch < CH; ++ch) {
+            ra[ch] = rc[ch];
+            rc[ch] = rb[ch];
+            elc[ch] = elb[ch], erc[ch] = erb[ch];
+            qw[ch][K1_OCT_PF - 1] = wd[ch], ql[ch][K1_OCT_PF - 1] = eld[ch], qr[ch][K1_OCT_PF - 1] = erd[ch];
+            rb[ch] = spread(qw[ch][0].x, qw[ch][0].y);
+            elb[ch] = ql[ch][0], erb[ch] = qr[ch][0];
+#pragma unroll
+            for (int i = 0; i + 1 < K1_OCT_PF; ++i)
+                qw[ch][i] = qw[ch][i + 1], ql[ch][i] = ql[ch][i + 1], qr[ch][i] = qr[ch][i + 1];
+        }
     };
 
     int y = y0;
@@ -447,17 +505,29 @@ __global__ void k_lut_proof(const uint8_t *__restrict__ lut, unsigned long long 
     if (bad) atomicAdd(mismatches, bad);
 }
 
-bool launch_grad_bin_oct(int bins, bool counts, const uint8_t *img, int64_t ip, int64_t ifs,
-                         int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g, const Scratch &sc,
-                         cudaStream_t st) {
+bool launch_grad_bin_oct(int bins, int c, bool counts, const uint8_t *img, int64_t ip, int64_t ics,
+                         int64_t ifs, int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g,
+                         const Scratch &sc, cudaStream_t st) {
     const int64_t units = (int64_t)g.n * g.nb1 * g.nc1;
     const unsigned nb = blocks_for_warps((units + 1) / 2);
-#define LAUNCH(NBv, CNT) \
-    k_grad_bin_oct<NBv, CNT><<<nb, K_THREADS, 0, st>>>(img, ip, ifs, bm, bp, bfs, g, sc)
-    if (bins == 8) {
-        if (counts) LAUNCH(8, true); else LAUNCH(8, false);
-    } else if (bins == 4) {
-        if (counts) LAUNCH(4, true); else LAUNCH(4, false);
+#define LAUNCH(NBv, CNT, CHv) \
+    k_grad_bin_oct<NBv, CNT, CHv><<<nb, K_THREADS, 0, st>>>(img, ip, ics, ifs, bm, bp, bfs, g, sc)
+    if (c == 1) {
+        if (bins == 8) {
+            if (counts) LAUNCH(8, true, 1); else LAUNCH(8, false, 1);
+        } else if (bins == 4) {
+            if (counts) LAUNCH(4, true, 1); else LAUNCH(4, false, 1);
+        } else {
+            return false;
+        }
+    } else if (c == 3) {
+        if (bins == 8) {
+            if (counts) LAUNCH(8, true, 3); else LAUNCH(8, false, 3);
+        } else if (bins == 4) {
+            if (counts) LAUNCH(4, true, 3); else LAUNCH(4, false, 3);
+        } else {
+            return false;
+        }
     } else {
         return false;
     }

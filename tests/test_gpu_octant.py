@@ -123,3 +123,28 @@ def test_octant_odd_shapes_match_oracle(shape):
     got = bm.data[:, :, :w].cpu().numpy().astype(np.int16)
     for i in range(n):
         assert np.array_equal(got[i], O.gradient_map(frames[i], O.build_lut(8)))
+
+
+@pytest.mark.parametrize("shape", [(2, 130, 264), (1, 72, 640)])
+def test_octant_rgb_channel_rule(shape):
+    """RGB: per-channel gradients, largest dx^2 + dy^2 wins, first channel on ties
+    (gradient.py:113-117), then the octant tests.  Channel 1 is the negative of
+    channel 0 (equal magnitudes, opposite gradients) and channel 2 repeats channel 0
+    on half the rows, so ties are everywhere; the rest is random."""
+    n, h, w = shape
+    rng = np.random.default_rng(w)
+    f = rng.integers(0, 256, size=(n, 3, h, w), dtype=np.uint8)
+    f[:, 1] = 255 - f[:, 0]
+    f[:, 2, : h // 2] = f[:, 0, : h // 2]
+    lut = H.build_lut(8)
+    frames = D.upload_frames(f)
+    box = {}
+
+    def run():
+        box["bm"] = grad_bin_device(frames, lut)
+
+    used, names = ran_octant_kernel(run)
+    assert used, sorted(set(names))
+    got = box["bm"].data[:, :, :w].cpu().numpy().astype(np.int16)
+    for i in range(n):
+        assert np.array_equal(got[i], O.gradient_map(f[i], O.build_lut(8)))
