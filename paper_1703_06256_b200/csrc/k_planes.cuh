@@ -697,7 +697,8 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
             // Full groups (every row computed and stored, no TMA ring): the same rows
             // without per-row guards, so the group compiles to straight-line code
             const bool fullg = !TMA && active && Y0 + rel + G <= Ycomp && Y0 + rel + G <= Ystore;
-            if (K2_FASTGROUP && VC == 4 && fullg) {  // measured: +0.3 % c2, -0.3 % c4 (VC = 8)
+            // measured: +0.3 % c2, +1 % c1; -0.3 % c4 (VC = 8), -4.5 % c5 (NW = 9: the duplicated body)
+            if (K2_FASTGROUP && VC == 4 && NW <= 4 && fullg) {
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
                     row_update(i);
