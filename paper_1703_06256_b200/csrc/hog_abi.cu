@@ -180,7 +180,8 @@ TileGeom make_geom(int n, int h, int w, int bins, bool fused, int stride, int ce
     if (s_env > 0 && R % s_env == 0) {
         g.S1 = s_env;
     } else if (s_env <= 0) {
-        const int64_t target = (int64_t)env_int("HOGB200_BIN_WAVES", 4) * 148 * 64;  // warps: ~4 full waves
+        // warps: ~2 full waves (B200: c3 1.179 -> 1.167 ms against 4 waves; c5, c1, c2 shard unchanged)
+        const int64_t target = (int64_t)env_int("HOGB200_BIN_WAVES", 2) * 148 * 64;
         // octant binning (N_b 4 / 8) counts in blocks of 8 rows: keep R1 % 8 == 0
         const bool oct = bins == 4 || bins == 8;
         while (R % (2 * g.S1) == 0 && R / (2 * g.S1) >= 16 && (!oct || (R / (2 * g.S1)) % 8 == 0) &&
