@@ -272,6 +272,21 @@ static void oct_subbands(TileGeom &g, int c, int smax) {
     g.nb1 = (g.h + g.R1 - 1) / g.R1;
 }
 
+// Row-bulk plane stores (k_planes RB): whole rows staged in shared memory and
+// written by one contiguous cp.async.bulk each.  Needs every strip of a row in
+// one CTA with all warps active, row-major contiguous rows (pp == bins * pns),
+// columns -7 .. w all written by the CTA (w % 8 == 0) and the two row slots
+// inside the two-CTAs-per-SM shared-memory budget.
+static void rowbulk_geom(TileGeom &g, const PlaneOut &po, int kr) {
+    g.RB = 0;
+    if (!env_int("HOGB200_ROWBULK", 1) || g.TMA || !g.PREG || g.NW != 4 || g.nss != 1 ||
+        g.ns != g.NWARP || !po.vec || po.pp != (int64_t)g.bins * po.pns || g.w % 8 != 0)
+        return;
+    g.RB = 1;
+    g.RBP = (int)po.pns;
+    if ((size_t)k2_smem_words(g, kr) * 4 > (size_t)K2_SMEM_BUDGET) g.RB = 0;
+}
+
 int check_pitch4(const void *p, int64_t pitch, int w, const char *what) {
     if (((uintptr_t)p & 3) != 0 || pitch % 4 != 0 || pitch < round_up(w, 4))
         return fail(HOG_EINVAL, "%s: need 4-byte aligned base and pitch %% 4 == 0, pitch >= %lld (got %lld)",
@@ -482,6 +497,7 @@ static int pipeline_impl(const uint8_t *img, int n, int c, int h, int w, int64_t
     g.ht = halo_top ? 1 : 0;
     g.hb = halo_bot ? 1 : 0;
     oct_subbands(g, c, g.S1);  // never more sub-bands than the scratch was sized for
+    rowbulk_geom(g, po, kr);
     Scratch sc{};
     size_t need = carve(g, nullptr, nullptr);
     if (scratch == nullptr || sbytes < need)

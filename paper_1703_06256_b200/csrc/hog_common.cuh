@@ -58,6 +58,8 @@ struct TileGeom {
     int TMA;    // plane rows staged in shared memory and written by TMA bulk stores
     int RING;   // TMA: staged plane rows in flight (ring slots)
     int SEGW;   // TMA: staged columns per bin row = NWARP*Ws + 8 (32-B aligned front pad)
+    int RB;     // whole plane rows staged in shared memory, one bulk copy per row (k_planes RB)
+    int RBP;    // RB: words per bin row in the slot (= the plane pitch pns)
 };
 
 // Scratch arrays (device), carved from the caller's scratch buffer.
@@ -103,6 +105,9 @@ struct GridOut {
 };
 
 constexpr int K2_G = 4;  // rows per phase-A/phase-B group
+#ifndef K2_RB_SLOTS
+#define K2_RB_SLOTS 3  // RB: staged plane rows in flight (shared-memory slots)
+#endif
 #ifndef K2_FASTGROUP
 #define K2_FASTGROUP 1  // guard-free code path for full row groups (k_planes.cuh)
 #endif
@@ -162,7 +167,7 @@ __host__ __device__ inline K2Smem k2_smem(const TileGeom &g, int kr) {
     m.ptop = m.Tsup + k2_r4(2 * NB);                             // [NWARP][NB][32][VC]
     m.ring = m.ptop + k2_r4(g.NWARP * NB * 32 * g.VC);           // [NWARP][KR][NB][32]
     m.stage = m.ring + k2_r4(g.NWARP * kr * NB * 32);             // TMA: [RING][bins][SEGW]
-    m.total = m.stage + (g.TMA ? g.RING * g.bins * g.SEGW : 0);
+    m.total = m.stage + (g.TMA ? g.RING * g.bins * g.SEGW : 0) + (g.RB ? K2_RB_SLOTS * g.bins * g.RBP : 0);
     return m;
 }
 

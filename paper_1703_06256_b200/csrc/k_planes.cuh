@@ -181,7 +181,7 @@ __device__ __forceinline__ void bin_rows(const FusedIn &fi, const TileGeom &g, i
 // cp.async.bulk per (bin, row) -- whole 32-B sectors, no LSU traffic -- then
 // releases the slot on empty[slot] once the TMA engine has read it.  The
 // compute warps synchronise among themselves with named barrier 1.
-template <int NW, int KR, int VC, bool VEC, int CH = 0, bool TMA = false, bool PR = false>
+template <int NW, int KR, int VC, bool VEC, int CH = 0, bool TMA = false, bool PR = false, bool RB = false>
 __global__ void __launch_bounds__(k2_maxt(NW, VC, PR), K2_MINB)
 k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, GridOut go,
          TileGeom g, Scratch sc, FusedIn fi) {
@@ -263,6 +263,12 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
         }
     }
     uint32_t tslot = 0, tphase = 0, trow = 0;  // TMA ring position of the next stored row
+    // RB: a CTA holds whole plane rows (every strip of the frame, nss == 1), the
+    // planes are row-major and contiguous per row (pp == bins * pns): each stored
+    // row (every bin, columns -7 .. P-8) is staged in one of two shared-memory
+    // slots and leaves as ONE contiguous cp.async.bulk, issued by thread 0
+    uint32_t rbslot = 0;
+    uint32_t *rbst = smem + lay.stage;  // RB: [K2_RB_SLOTS][bins][pns] words
 
     const int Y0 = b * g.R;
     const int Ystore = min(Y0 + g.R - 1, g.h);
@@ -457,6 +463,42 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                 if (lane == 0) mbar_arrive(full + tslot);
                 ++trow;
                 if (++tslot == (uint32_t)g.RING) tslot = 0, tphase ^= 1u;
+                return;
+            }
+            if constexpr (RB) {
+                uint32_t *slotp = rbst + rbslot * g.bins * pns;
+                if (s == 0 && lane < NB && (lane < NB - 1 || !odd)) {  // columns -7..0
+                    uint4 *z = reinterpret_cast<uint4 *>(slotp + lane * pns);
+                    z[0] = make_uint4(0, 0, 0, 0);
+                    z[1] = make_uint4(0, 0, 0, 0);
+                }
+                if (st) {
+                    uint32_t *sp = slotp + X0 + 7;  // slot column of plane column X0
+#pragma unroll
+                    for (int n = 0; n < NB; ++n) {
+                        if (n < NB - 1 || !odd) {
+                            uint32_t vals[VC];
+#pragma unroll
+                            for (int k = 0; k < VC; ++k)
+                                vals[k] = preg[PREG ? n : 0][PREG ? k : 0] + Lacc[n] + half16(Q[n >> 1][k], n & 1);
+#pragma unroll
+                            for (int k = 0; k < VC; k += 4)
+                                *reinterpret_cast<uint4 *>(sp + n * pns + k) =
+                                    make_uint4(vals[k], vals[k + 1], vals[k + 2], vals[k + 3]);
+                        }
+                    }
+                }
+                fence_proxy_async();  // this thread's slot writes -> the async proxy
+                // the copy issued K2_RB_SLOTS - 1 rows ago has read its slot, so the
+                // slot the next row writes is free once everyone passes the barrier
+                if (threadIdx.x == 0) bulk_wait_read<K2_RB_SLOTS - 2>();
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    bulk_store(prow - X0 - 7, slotp, (uint32_t)(g.bins * pns * 4));
+                    bulk_commit();
+                }
+                if (++rbslot == (uint32_t)K2_RB_SLOTS) rbslot = 0;
+                prow += pp;
                 return;
             }
             if (s == 0 && lane < NB && (lane < NB - 1 || !odd)) {
@@ -724,18 +766,21 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
         }
         csync();
     }
+    if constexpr (RB) {
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
 }
 
-template <int NW, int KR, int VC, bool VEC, int CH, bool TMA = false, bool PR = false>
+template <int NW, int KR, int VC, bool VEC, int CH, bool TMA = false, bool PR = false, bool RB = false>
 void launch_planes_vc(const int8_t *bm, int64_t bp, int64_t bfs, const PlaneOut &po,
                       const GridOut &go, const TileGeom &g, const Scratch &sc, const FusedIn &fi,
                       cudaStream_t st) {
     const size_t smem = (size_t)k2_smem_words(g, KR) * 4;
     static size_t configured[HOG_MAX_DEVICES] = {};  // per instantiation and device
     if (smem_optin_needed(configured, smem))
-        cudaFuncSetAttribute(k_planes<NW, KR, VC, VEC, CH, TMA, PR>,
+        cudaFuncSetAttribute(k_planes<NW, KR, VC, VEC, CH, TMA, PR, RB>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_planes<NW, KR, VC, VEC, CH, TMA, PR>
+    k_planes<NW, KR, VC, VEC, CH, TMA, PR, RB>
         <<<(unsigned)((int64_t)g.n * g.nb2), 32 * (g.NWARP + (TMA ? 1 : 0)), smem, st>>>(
             bm, bp, bfs, po, go, g, sc, fi);
 }
@@ -769,6 +814,10 @@ void launch_planes_kr(int ch, const int8_t *bm, int64_t bp, int64_t bfs, const P
     }
     if constexpr (2 * NW * 4 <= 32) {
         if (g.PREG) {
+            if constexpr (NW == 4) {
+                if (g.RB && po.vec)
+                    return launch_planes_vc<NW, KR, 4, true, 0, false, true, true>(bm, bp, bfs, po, go, g, sc, fi, st);
+            }
             if (po.vec)
                 return launch_planes_vc<NW, KR, 4, true, 0, false, true>(bm, bp, bfs, po, go, g, sc, fi, st);
             return launch_planes_vc<NW, KR, 4, false, 0, false, true>(bm, bp, bfs, po, go, g, sc, fi, st);
