@@ -108,6 +108,9 @@ constexpr int K2_G = 4;  // rows per phase-A/phase-B group
 #ifndef K2_RB_SLOTS
 #define K2_RB_SLOTS 3  // RB: staged plane rows in flight (shared-memory slots)
 #endif
+#ifndef K2_RB_DECOUPLED
+#define K2_RB_DECOUPLED 0  // RB: 1 = producer/consumer named barriers instead of a CTA barrier per row (c2 -0.8 %, shard +1.2 %)
+#endif
 #ifndef K2_FASTGROUP
 #define K2_FASTGROUP 1  // guard-free code path for full row groups (k_planes.cuh)
 #endif
@@ -229,6 +232,9 @@ __device__ __forceinline__ void fence_proxy_async() {
 // barrier over the first `threads` threads of the CTA (the compute warps)
 __device__ __forceinline__ void named_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int threads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {

@@ -267,8 +267,9 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
     // planes are row-major and contiguous per row (pp == bins * pns): each stored
     // row (every bin, columns -7 .. P-8) is staged in one of two shared-memory
     // slots and leaves as ONE contiguous cp.async.bulk, issued by thread 0
-    uint32_t rbslot = 0;
+    uint32_t rbslot = 0, rbn = 0;  // RB: slot of the next stored row, rows stored so far
     uint32_t *rbst = smem + lay.stage;  // RB: [K2_RB_SLOTS][bins][pns] words
+    const uint32_t rbrows = (uint32_t)(min(b * g.R + g.R - 1, g.h) - b * g.R + 1);  // rows this CTA stores
 
     const int Y0 = b * g.R;
     const int Ystore = min(Y0 + g.R - 1, g.h);
@@ -467,6 +468,11 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
             }
             if constexpr (RB) {
                 uint32_t *slotp = rbst + rbslot * g.bins * pns;
+#if K2_RB_DECOUPLED
+                // the slot is free once warp 0 has waited for the copy that read it
+                // (EMPTY, barrier 2, arrived by warp 0 one row earlier)
+                if (warp != 0 && rbn > 0) named_sync(2, 32 * nwarp);
+#endif
                 if (s == 0 && lane < NB && (lane < NB - 1 || !odd)) {  // columns -7..0
                     uint4 *z = reinterpret_cast<uint4 *>(slotp + lane * pns);
                     z[0] = make_uint4(0, 0, 0, 0);
@@ -489,6 +495,24 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                     }
                 }
                 fence_proxy_async();  // this thread's slot writes -> the async proxy
+#if K2_RB_DECOUPLED
+                // FULL (barrier 1): warps 1.. arrive and go on; warp 0 waits for every
+                // warp's part of the row, issues the copy, and then tells the others
+                // (EMPTY) that the slot of the next row is free: the copy issued
+                // K2_RB_SLOTS - 1 rows ago has been read
+                if (warp == 0) {
+                    if (lane == 0) bulk_wait_read<K2_RB_SLOTS - 2>();
+                    named_sync(1, 32 * nwarp);
+                    if (lane == 0) {
+                        bulk_store(prow - X0 - 7, slotp, (uint32_t)(g.bins * pns * 4));
+                        bulk_commit();
+                    }
+                    if (rbn + 1 < rbrows) named_arrive(2, 32 * nwarp);
+                } else {
+                    named_arrive(1, 32 * nwarp);
+                }
+                ++rbn;
+#else
                 // the copy issued K2_RB_SLOTS - 1 rows ago has read its slot, so the
                 // slot the next row writes is free once everyone passes the barrier
                 if (threadIdx.x == 0) bulk_wait_read<K2_RB_SLOTS - 2>();
@@ -497,6 +521,7 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                     bulk_store(prow - X0 - 7, slotp, (uint32_t)(g.bins * pns * 4));
                     bulk_commit();
                 }
+#endif
                 if (++rbslot == (uint32_t)K2_RB_SLOTS) rbslot = 0;
                 prow += pp;
                 return;
