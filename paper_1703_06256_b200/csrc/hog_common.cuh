@@ -105,8 +105,11 @@ struct GridOut {
 };
 
 constexpr int K2_G = 4;  // rows per phase-A/phase-B group
+#ifndef K2_RB_ROWS
+#define K2_RB_ROWS 2  // RB: plane rows per staging slot (one bulk copy and one barrier per slot)
+#endif
 #ifndef K2_RB_SLOTS
-#define K2_RB_SLOTS 3  // RB: staged plane rows in flight (shared-memory slots)
+#define K2_RB_SLOTS (K2_RB_ROWS == 1 ? 3 : 2)  // RB: staging slots in flight
 #endif
 #ifndef K2_RB_DECOUPLED
 #define K2_RB_DECOUPLED 0  // RB: 1 = producer/consumer named barriers instead of a CTA barrier per row (c2 -0.8 %, shard +1.2 %)
@@ -168,9 +171,11 @@ __host__ __device__ inline K2Smem k2_smem(const TileGeom &g, int kr) {
     m.vtot = m.Lsup + k2_r4(2 * g.Lrows * g.NWp);                // [NWARP][NB]
     m.Tsup = m.vtot + k2_r4(g.NWARP * NB);                       // [2][NB]
     m.ptop = m.Tsup + k2_r4(2 * NB);                             // [NWARP][NB][32][VC]
-    m.ring = m.ptop + k2_r4(g.NWARP * NB * 32 * g.VC);           // [NWARP][KR][NB][32]
+    // (the register top-row variant keeps ptop in registers: no shared copy)
+    m.ring = m.ptop + ((g.PREG && !g.TMA) ? 0 : k2_r4(g.NWARP * NB * 32 * g.VC));  // [NWARP][KR][NB][32]
     m.stage = m.ring + k2_r4(g.NWARP * kr * NB * 32);             // TMA: [RING][bins][SEGW]
-    m.total = m.stage + (g.TMA ? g.RING * g.bins * g.SEGW : 0) + (g.RB ? K2_RB_SLOTS * g.bins * g.RBP : 0);
+    m.total = m.stage + (g.TMA ? g.RING * g.bins * g.SEGW : 0) +
+              (g.RB ? K2_RB_SLOTS * K2_RB_ROWS * g.bins * g.RBP : 0);
     return m;
 }
 

@@ -267,8 +267,9 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
     // planes are row-major and contiguous per row (pp == bins * pns): each stored
     // row (every bin, columns -7 .. P-8) is staged in one of two shared-memory
     // slots and leaves as ONE contiguous cp.async.bulk, issued by thread 0
-    uint32_t rbslot = 0, rbn = 0;  // RB: slot of the next stored row, rows stored so far
-    uint32_t *rbst = smem + lay.stage;  // RB: [K2_RB_SLOTS][bins][pns] words
+    uint32_t rbslot = 0, rbn = 0, rbq = 0;  // RB: slot, rows stored so far, row within the slot
+    uint32_t *rbst = smem + lay.stage;  // RB: [K2_RB_SLOTS][K2_RB_ROWS][bins][pns] words
+    int32_t *rbdst = nullptr;           // RB: plane address of the slot's first row (column -7)
     const uint32_t rbrows = (uint32_t)(min(b * g.R + g.R - 1, g.h) - b * g.R + 1);  // rows this CTA stores
 
     const int Y0 = b * g.R;
@@ -467,13 +468,17 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                 return;
             }
             if constexpr (RB) {
-                uint32_t *slotp = rbst + rbslot * g.bins * pns;
-#if K2_RB_DECOUPLED
+                const int64_t rowsz = (int64_t)g.bins * pns;  // words of one staged row
+                uint32_t *slotp = rbst + (rbslot * K2_RB_ROWS + rbq) * rowsz;
+                if (rbq == 0) rbdst = prow - X0 - 7;
+#if K2_RB_DECOUPLED && K2_RB_ROWS == 1
                 // the slot is free once warp 0 has waited for the copy that read it
                 // (EMPTY, barrier 2, arrived by warp 0 one row earlier)
                 if (warp != 0 && rbn > 0) named_sync(2, 32 * nwarp);
 #endif
-                if (s == 0 && lane < NB && (lane < NB - 1 || !odd)) {  // columns -7..0
+                // columns -7..0 of every bin are zero: written once per slot row at the
+                // CTA's first rows (nothing else writes them)
+                if (rbn < (uint32_t)(K2_RB_SLOTS * K2_RB_ROWS) && s == 0 && lane < NB && (lane < NB - 1 || !odd)) {
                     uint4 *z = reinterpret_cast<uint4 *>(slotp + lane * pns);
                     z[0] = make_uint4(0, 0, 0, 0);
                     z[1] = make_uint4(0, 0, 0, 0);
@@ -495,7 +500,7 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                     }
                 }
                 fence_proxy_async();  // this thread's slot writes -> the async proxy
-#if K2_RB_DECOUPLED
+#if K2_RB_DECOUPLED && K2_RB_ROWS == 1
                 // FULL (barrier 1): warps 1.. arrive and go on; warp 0 waits for every
                 // warp's part of the row, issues the copy, and then tells the others
                 // (EMPTY) that the slot of the next row is free: the copy issued
@@ -513,14 +518,22 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                 }
                 ++rbn;
 #else
-                // the copy issued K2_RB_SLOTS - 1 rows ago has read its slot, so the
-                // slot the next row writes is free once everyone passes the barrier
-                if (threadIdx.x == 0) bulk_wait_read<K2_RB_SLOTS - 2>();
-                __syncthreads();
-                if (threadIdx.x == 0) {
-                    bulk_store(prow - X0 - 7, slotp, (uint32_t)(g.bins * pns * 4));
-                    bulk_commit();
+                // a slot of K2_RB_ROWS rows leaves when full (or at the CTA's last row):
+                // the copy issued K2_RB_SLOTS - 1 slots ago has read its slot, so the
+                // slot written next is free once everyone passes the barrier
+                ++rbn;
+                if (++rbq == (uint32_t)K2_RB_ROWS || rbn == rbrows) {
+                    if (threadIdx.x == 0) bulk_wait_read<K2_RB_SLOTS - 2>();
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        bulk_store(rbdst, rbst + rbslot * K2_RB_ROWS * rowsz, (uint32_t)(rbq * rowsz * 4));
+                        bulk_commit();
+                    }
+                    rbq = 0;
+                    if (++rbslot == (uint32_t)K2_RB_SLOTS) rbslot = 0;
                 }
+                prow += pp;
+                return;
 #endif
                 if (++rbslot == (uint32_t)K2_RB_SLOTS) rbslot = 0;
                 prow += pp;
