@@ -194,6 +194,16 @@ class HogPipeline:
         auto = self.auto_band_rows()
         cands = [auto] + [r for r in (32, 40, 48, 64, 80, 96, 128)
                           if r != auto and r <= max(D.round_up(self.h + 1, 8), 32)]
+        # plus the two band heights whose plane-kernel grid (frames x bands CTAs, two
+        # per SM) fills its last wave best: small batches lose most to the tail
+        # (c2's 64-frame shard of an 8-GPU run)
+        slots = 2 * 148
+        def fill(r):
+            ctas = self.n * (self.h // r + 1)
+            return ctas / (-(-ctas // slots) * slots)
+        extra = sorted((r for r in range(24, 161, 8) if r not in cands and r <= self.h + 1),
+                       key=lambda r: (-fill(r), -r))[:2]
+        cands += extra
         stream = t.cuda.current_stream(self.device)
         times = {}
         for r in cands:
