@@ -280,7 +280,8 @@ static void oct_subbands(TileGeom &g, int c, int smax) {
 static void rowbulk_geom(TileGeom &g, const PlaneOut &po, int kr) {
     g.RB = 0;
     if (!env_int("HOGB200_ROWBULK", 1) || g.TMA || !g.PREG || g.NW != 4 || g.nss != 1 ||
-        g.ns != g.NWARP || !po.vec || po.pp != (int64_t)g.bins * po.pns || g.w % 8 != 0)
+        g.ns != g.NWARP || !po.vec || po.pp != (int64_t)g.bins * po.pns || g.w % 8 != 0 ||
+        po.pns != (int64_t)g.w + 8)  // every staged column (-7 .. w) is written each row
         return;
     g.RB = 1;
     g.RBP = (int)po.pns;
