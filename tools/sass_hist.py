@@ -12,8 +12,10 @@ import sys
 LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_1703_06256_b200/libhogb200.so"
 # (label, mangled-name pattern): the variants the BASELINE configs run
 KERNELS = [
-    ("k_planes c2 (NW=4, lattice step 4, 4 cols/lane, register top row)",
-     r"k_planesILi4ELi2ELi4ELb1ELi0ELb0ELb1EE"),
+    ("k_planes c2 (NW=4, lattice step 4, 4 cols/lane, register top row, row-bulk TMA stores)",
+     r"k_planesILi4ELi2ELi4ELb1ELi0ELb0ELb1ELb1EE"),
+    ("k_planes c2 without row-bulk stores (HOGB200_ROWBULK=0: per-thread st.global)",
+     r"k_planesILi4ELi2ELi4ELb1ELi0ELb0ELb1ELb0EE"),
     ("k_planes c4 (NW=4, lattice step 8, 8 cols/lane)", r"k_planesILi4ELi1ELi8ELb1ELi0ELb0ELb0EE"),
     ("k_planes c5 (NW=9, 18 bins, lattice step 8)", r"k_planesILi9ELi1ELi4ELb1ELi0ELb0ELb0EE"),
     ("k_grad_bin_oct gray, 8 bins, counts (c1/c2: fp16x2 octant sign tests, no table gather)",
