@@ -264,6 +264,75 @@ static bool oct_enabled(int c) {
     return v >= 2 || (v == 1 && c == 1);
 }
 
+// Small batches (config c1's single frame; a few frames per GPU): one thread
+// per column walks ~2H/R1 sub-bands one dependent round of loads per 8 (c1: 75
+// sub-bands, 11 us).  Here SPL threads share a column: each sums a contiguous
+// run of sub-bands, the group exchanges exclusive prefixes by shuffle, and each
+// thread emits the bands whose first sub-band falls in its run; the bands that
+// start at or past the last row get the column total.  Same V as k_scan_cols.
+template <int NWB, int NW, int SPL>
+__global__ void k_scan_cols_split(TileGeom g, Scratch sc) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = (int)(threadIdx.x % SPL);
+    const int64_t col = t / SPL;
+    const bool ok = col < (int64_t)g.n * g.Wc;
+    const int f = ok ? (int)(col / g.Wc) : 0, x = ok ? (int)(col % g.Wc) : 0;
+    const int ch = (g.nb1 + SPL - 1) / SPL;
+    const int s0 = min(l * ch, g.nb1), s1 = min(s0 + ch, g.nb1);
+    const uint32_t *__restrict__ Cf = sc.C + (int64_t)f * g.nb1 * g.Wc * NWB + (int64_t)x * NWB;
+    auto add_sub = [&](uint32_t (&acc)[NW], int sb) {
+        uint32_t c[NWB];
+#pragma unroll
+        for (int w = 0; w < NWB; ++w) c[w] = __ldg(Cf + (int64_t)sb * g.Wc * NWB + w);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) acc[w] += widen_half(c[w >> 1], w & 1);
+    };
+    uint32_t sum[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) sum[w] = 0;
+    for (int sb = s0; sb < s1; ++sb) add_sub(sum, sb);
+    // exclusive prefix over the column's SPL threads, plus the slab carry
+    uint32_t run[NW], total[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        uint32_t inc = sum[w];
+#pragma unroll
+        for (int d = 1; d < SPL; d <<= 1) {
+            const uint32_t v = __shfl_up_sync(FULL, inc, d, SPL);
+            if (l >= d) inc += v;
+        }
+        run[w] = inc - sum[w];
+        total[w] = __shfl_sync(FULL, inc, SPL - 1, SPL);
+    }
+    if (sc.base && ok && x < g.w) {  // slab mode: counts above the slab's first plane row
+        const int32_t *bs = sc.base + (int64_t)f * sc.base_fs + x;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t lo = (uint32_t)bs[(int64_t)(2 * w) * g.w];
+            const uint32_t hi = 2 * w + 1 < g.bins ? (uint32_t)bs[(int64_t)(2 * w + 1) * g.w] : 0u;
+            run[w] += lo | (hi << 16);
+            total[w] += lo | (hi << 16);
+        }
+    }
+    if (!ok) return;
+    uint32_t *__restrict__ Vf = sc.V + (int64_t)f * g.nb2 * g.Wc * g.NWp + (int64_t)x * g.NWp;
+    auto store_v = [&](int b, const uint32_t (&v)[NW]) {
+        uint4 *vp = reinterpret_cast<uint4 *>(Vf + (int64_t)b * g.Wc * g.NWp);
+#pragma unroll
+        for (int q = 0; q < (NW + 3) / 4; ++q)
+            vp[q] = make_uint4(v[4 * q], 4 * q + 1 < NW ? v[4 * q + 1] : 0u,
+                               4 * q + 2 < NW ? v[4 * q + 2] : 0u, 4 * q + 3 < NW ? v[4 * q + 3] : 0u);
+    };
+    // bands whose first sub-band b*S1 lies in [s0, s1)
+    int sb = s0;
+    for (int b = (s0 + g.S1 - 1) / g.S1; b < g.nb2 && b * g.S1 < s1; ++b) {
+        for (; sb < b * g.S1; ++sb) add_sub(run, sb);
+        store_v(b, run);
+    }
+    if (l == SPL - 1)  // bands starting at or past the last row
+        for (int b = (g.nb1 + g.S1 - 1) / g.S1; b < g.nb2; ++b) store_v(b, total);
+}
+
 template <int NWB>
 void grad_bin_t(int c, bool counts, const uint8_t *img, int64_t ip, int64_t ics, int64_t ifs,
                 const uint8_t *lut, int8_t *bm, int64_t bp, int64_t bfs, const TileGeom &g,
@@ -332,6 +401,14 @@ void launch_column_counts(const int8_t *bm, int64_t bp, int64_t bfs, int n, int 
 template <int NW>
 void scan_t(const TileGeom &g, const Scratch &sc, cudaStream_t st) {
     constexpr int NWB = (2 * NW + 3) / 4;
+    constexpr int SPL = 8;
+    const char *e = getenv("HOGB200_SCAN_SPLIT");  // 0: always one thread per column (A/B)
+    const bool split_ok = !(e && *e == '0');
+    // long per-column chains on a grid under ~1 wave: split them
+    if (split_ok && g.nb1 >= 16 && (int64_t)g.n * g.Wc * SPL <= (int64_t)148 * 2048) {
+        k_scan_cols_split<NWB, NW, SPL><<<blocks_for((int64_t)g.n * g.Wc * SPL, 256), 256, 0, st>>>(g, sc);
+        return;
+    }
     k_scan_cols<NWB, NW><<<blocks_for((int64_t)g.n * g.Wc, 256), 256, 0, st>>>(g, sc);
 }
 
