@@ -6,7 +6,7 @@ NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xptxas -v
 CSRC := paper_1703_06256_b200/csrc
 OBJDIR := build/obj
 LIB := paper_1703_06256_b200/libhogb200.so
-UNITS := hog_abi k_bin k_bin_oct k_planes_a k_planes_b k_planes_c k_planes_d k_window k_scores k_detect k_rect
+UNITS := hog_abi k_bin k_bin_oct k_planes_a k_planes_b k_planes_c k_planes_d k_window k_scores k_scores_i8 k_detect k_rect
 OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(UNITS)))
 HDRS := $(CSRC)/hog_common.cuh $(CSRC)/k_planes.cuh include/hogb200.h
 

@@ -46,6 +46,7 @@ typedef struct CUstream_st *hog_stream_t; /* == cudaStream_t */
 #define HOG_OK 0
 #define HOG_EINVAL 1
 #define HOG_ECUDA 2
+#define HOG_ERANGE 3 /* weights the integer score path cannot hold exactly */
 
 /* hog_pipeline stages (bitmask; 0 = all) */
 #define HOG_STAGE_BIN 1    /* gradient + LUT binning + per-band column counts */
@@ -196,6 +197,29 @@ int hog_scores_lattice(const int32_t *grid, const double *den, int n, int ncy, i
 int hog_scores_lattice_u8(const uint8_t *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
                           int cells_x, int cells_y, int k, const double *weights, double bias,
                           double *scores, hog_stream_t stream);
+
+/* Exact window scores on the integer tensor cores (detector.py:140-154,
+ * descriptor.py:107-118; same windows and weights layout as
+ * hog_scores_lattice_u8 with k = 1, i.e. stride = cell, cells_x = 8,
+ * cells_y <= 16, bins <= HOG_I8_MAX_BINS).  The dot of a window's counts with
+ * the weights is evaluated exactly in integers and rounded once to float64,
+ * then the bias is added (the reference: float64 ddot + bias).
+ * hog_scores_i8_prepare (host only, no CUDA) writes each weight as an integer
+ * times 2^-F in `*digits` signed base-256 digits, laid out as tensor-core
+ * fragments in `frag` (hog_scores_i8_frag_bytes(bins) host bytes, to be
+ * copied to a 16-byte aligned device buffer).  Exact when the weights span
+ * at most 47 bits (float32-valued weights span ~37); wider (float64) weights
+ * are rounded to multiples of 2^(e - 46), |w| < 2^e the largest (error <= 2^(e - 47)),
+ * of the size of float64 rounding in the dot itself.  HOG_ERANGE for non-finite
+ * or vanishingly small (< 2^-950) weights: use hog_scores_lattice_u8. */
+#define HOG_I8_MAX_BINS 20
+#define HOG_I8_MAX_DIGITS 6
+size_t hog_scores_i8_frag_bytes(int bins);
+int hog_scores_i8_prepare(const double *weights, int cells_x, int cells_y, int bins, void *frag,
+                          int *digits, double *scale);
+int hog_scores_lattice_i8(const uint8_t *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
+                          int cells_x, int cells_y, const void *frag, int digits, double scale,
+                          double bias, double *scores, hog_stream_t stream);
 
 /* detector.py:202-221 (_resize_bilinear): separable bilinear, pixel centres
  * aligned, float64 in the reference's operation order (no FMA contraction),

@@ -13,7 +13,7 @@ from .errors import FastHogError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HOGB200_LIB") or os.path.join(_HERE, "libhogb200.so")
 
-HOG_OK, HOG_EINVAL, HOG_ECUDA = 0, 1, 2
+HOG_OK, HOG_EINVAL, HOG_ECUDA, HOG_ERANGE = 0, 1, 2, 3
 STAGE_BIN, STAGE_SCAN, STAGE_PLANES, STAGE_ALL, STAGE_GRID_U8 = 1, 2, 4, 7, 8
 
 # (name, restype, argtypes) -- must match include/hogb200.h
@@ -40,6 +40,9 @@ SIGNATURES = {
                                  _P, _D, _P, _P, _P]),
     "hog_scores_lattice": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _D, _P, _P]),
     "hog_scores_lattice_u8": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _D, _P, _P]),
+    "hog_scores_i8_frag_bytes": (_SZ, [_I]),
+    "hog_scores_i8_prepare": (_I, [_P, _I, _I, _I, _P, _P, _P]),
+    "hog_scores_lattice_i8": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _D, _D, _P, _P]),
     "hog_resize_bilinear": (_I, [_P, _I, _I, _I, _I, _L, _L, _L, _I, _I, _D, _D,
                                  _P, _L, _L, _L, _P]),
     "hog_integral16": (_I, [_P, _I, _I, _I, _L, _L, _I, _P, _L, _L, _L, _P]),

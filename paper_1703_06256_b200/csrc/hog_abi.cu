@@ -21,7 +21,11 @@
 //   column) while it bins the image, and k_scan_cols turns those counts into
 //   the column counts above every band.  When the scan lattice is regular,
 //   k_planes also emits the cell-histogram grid from the plane values it
+#include <climits>
+#include <cmath>
+#include <cstring>
 #include <map>
+#include <vector>
 #include <mutex>
 
 #include "hog_common.cuh"
@@ -677,6 +681,103 @@ int hog_scores_lattice_u8(const uint8_t *grid, int n, int ncy, int ncx, int bins
     launch_scores_rows_u8(grid, n, ncy, ncx, bins, noy, nox, cells_y, k, wts, bias, scores,
                           (cudaStream_t)stream);
     return check_launch("hog_scores_lattice_u8");
+}
+
+// ---- exact integer-tensor-core scores (k_scores_i8.cu) ----------------------
+
+size_t hog_scores_i8_frag_bytes(int bins) {
+    if (bins < 1 || bins > HOG_I8_MAX_BINS) return 0;
+    return (size_t)HOG_I8_MAX_DIGITS * scores_i8_ks(bins) * 32 * 16;
+}
+
+int hog_scores_i8_prepare(const double *w, int cells_x, int cells_y, int bins, void *frag,
+                          int *digits, double *scale) {
+    g_err.clear();
+    if (!w || !frag || !digits || !scale) return fail(HOG_EINVAL, "null pointer");
+    if (cells_x != 8) return fail(HOG_EINVAL, "integer scores are built for 8 cells across, got %d", cells_x);
+    if (cells_y < 1 || cells_y > 16) return fail(HOG_EINVAL, "integer scores need 1..16 cell rows, got %d", cells_y);
+    if (bins < 1 || bins > HOG_I8_MAX_BINS)
+        return fail(HOG_EINVAL, "integer scores need 1..%d bins, got %d", HOG_I8_MAX_BINS, bins);
+    const int nw = cells_y * cells_x * bins;
+    // F: every weight times 2^F is an integer (the lowest set mantissa bit of any weight)
+    int lsb = INT_MAX, top = INT_MIN;
+    for (int i = 0; i < nw; ++i) {
+        const double v = w[i];
+        if (!std::isfinite(v)) return fail(HOG_ERANGE, "weight %d is not finite", i);
+        if (v == 0.0) continue;
+        int e;
+        const double m = std::frexp(std::fabs(v), &e);  // |v| = m 2^e, m in [0.5, 1)
+        uint64_t M = (uint64_t)std::ldexp(m, 53);        // 53-bit integer mantissa
+        const int tz = __builtin_ctzll(M);
+        lsb = std::min(lsb, e - 53 + tz);
+        top = std::max(top, e);
+    }
+    // exact when every W fits 47 bits (float32-valued weights span ~37); wider
+    // weights (float64 mantissas) are rounded to the grid 2^(top - 46): an error
+    // <= 2^(top - 47) per weight, the size of float64 rounding in the dot itself
+    int F = lsb == INT_MAX ? 0 : -lsb;
+    const int maxbits = 8 * HOG_I8_MAX_DIGITS - 1;
+    const bool exact = lsb == INT_MAX || top + F <= maxbits;
+    if (!exact) F = maxbits - 1 - top;
+    if (F > 1000) return fail(HOG_ERANGE, "weights too small for the integer path (2^-%d)", F);
+    const int bitsW = lsb == INT_MAX ? 0 : top + F;
+    int S = 1;
+    while (8 * S - 1 < bitsW) ++S;
+    const int KS = scores_i8_ks(bins), P = 4 * KS;
+    std::vector<int8_t> d((size_t)HOG_I8_MAX_DIGITS * nw, 0);  // d[s][i]
+    for (int i = 0; i < nw; ++i) {
+        long long W = std::llround(std::ldexp(w[i], F));
+        if (exact && (double)W != std::ldexp(w[i], F)) return fail(HOG_ERANGE, "weight %d is not exact at 2^-%d", i, F);
+        for (int s = 0; s < S; ++s) {
+            long long r = ((W % 256) + 256) % 256;
+            if (r >= 128) r -= 256;
+            d[(size_t)s * nw + i] = (int8_t)r;
+            W = (W - r) / 256;
+        }
+        if (W != 0) return fail(HOG_ERANGE, "weight %d does not fit %d digits", i, S);
+    }
+    // mma.sync m16n8k32 A fragments: [s][ks][lane] x 4 registers; register r of
+    // lane (g, t) holds row g + 8 (r & 1), k = 32 ks + 4 t + 16 (r >> 1) .. + 3
+    const int Sk = std::max(S, 4);
+    uint32_t *out = static_cast<uint32_t *>(frag);
+    std::memset(frag, 0, hog_scores_i8_frag_bytes(bins));
+    for (int s = 0; s < S; ++s)
+        for (int ks = 0; ks < KS; ++ks)
+            for (int lane = 0; lane < 32; ++lane)
+                for (int r = 0; r < 4; ++r) {
+                    const int row = (lane >> 2) + 8 * (r & 1);
+                    const int k0 = 32 * ks + 4 * (lane & 3) + 16 * (r >> 1);
+                    uint32_t word = 0;
+                    for (int q = 0; q < 4; ++q) {
+                        const int k = k0 + q, cx = k / P, n = k % P;
+                        if (row < cells_y && cx < cells_x && n < bins)
+                            word |= (uint32_t)(uint8_t)d[(size_t)s * nw + (row * cells_x + cx) * bins + n] << (8 * q);
+                    }
+                    out[(((size_t)s * KS + ks) * 32 + lane) * 4 + r] = word;
+                }
+    *digits = Sk;
+    *scale = std::ldexp(1.0, -F);
+    return HOG_OK;
+}
+
+int hog_scores_lattice_i8(const uint8_t *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
+                          int cells_x, int cells_y, const void *frag, int digits, double scale,
+                          double bias, double *scores, hog_stream_t stream) {
+    g_err.clear();
+    if (n < 1 || noy < 1 || nox < 1 || !grid || !frag || !scores) return fail(HOG_EINVAL, "bad arguments");
+    if (bins < 1 || bins > HOG_I8_MAX_BINS)
+        return fail(HOG_EINVAL, "integer scores need 1..%d bins, got %d", HOG_I8_MAX_BINS, bins);
+    if (cells_x != 8) return fail(HOG_EINVAL, "integer scores are built for 8 cells across, got %d", cells_x);
+    if (cells_y < 1 || cells_y > 16) return fail(HOG_EINVAL, "integer scores need 1..16 cell rows, got %d", cells_y);
+    if (digits < 4 || digits > HOG_I8_MAX_DIGITS) return fail(HOG_EINVAL, "digits must be 4..%d, got %d", HOG_I8_MAX_DIGITS, digits);
+    if ((int64_t)(noy - 1) + (cells_y - 1) >= ncy || (int64_t)(nox - 1) + 7 >= ncx)
+        return fail(HOG_EINVAL, "window grid exceeds the cell lattice");
+    if (((uintptr_t)frag & 15) != 0) return fail(HOG_EINVAL, "fragments must be 16-byte aligned");
+    if ((bins % 4 == 0 && ((uintptr_t)grid & 3)) || (bins % 2 == 0 && ((uintptr_t)grid & 1)))
+        return fail(HOG_EINVAL, "grid pointer misaligned for %d bins", bins);
+    launch_scores_i8(grid, n, ncy, ncx, bins, noy, nox, frag, digits, scale, bias, scores,
+                     (cudaStream_t)stream);
+    return check_launch("hog_scores_lattice_i8");
 }
 
 int hog_resize_bilinear(const uint8_t *src, int n, int c, int h, int w, int64_t sp, int64_t scs,

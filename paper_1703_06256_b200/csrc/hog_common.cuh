@@ -400,6 +400,10 @@ void launch_scores_rows(const int32_t *grid, int n, int ncy, int ncx, int bins, 
 void launch_scores_rows_u8(const uint8_t *grid, int n, int ncy, int ncx, int bins, int noy,
                            int nox, int cells_y, int k, const double *wts, double bias,
                            double *scores, cudaStream_t st);
+int scores_i8_ks(int bins);
+void launch_scores_i8(const uint8_t *grid, int n, int ncy, int ncx, int bins, int noy, int nox,
+                      const void *wfrag, int digits, double scale, double bias, double *scores,
+                      cudaStream_t st);
 void launch_resize(const uint8_t *src, int n, int c, int h, int w, int64_t sp, int64_t scs,
                    int64_t sfs, int nh, int nw, double ry, double rx, uint8_t *dst, int64_t dp,
                    int64_t dcs, int64_t dfs, cudaStream_t st);

@@ -359,6 +359,72 @@ k_resize(const uint8_t *__restrict__ src, int c, int h, int w, int64_t sp, int64
     }
 }
 
+// Row-shared resize for downscales up to 2x (pyramid levels 1-3 of c5 hold
+// three quarters of the level pixels): per output row the CTA first forms the
+// vertical mix `rows` (detector.py:216) of every source column its 256 output
+// columns read -- once per column, in shared memory, from coalesced byte
+// loads -- and then each thread mixes its column's two entries (:217).  Same
+// float64 operations in the same order as k_resize; bytes become doubles by a
+// shared 256-entry table, rint + clip by one add of 1.5 * 2^52 (round half to
+// even; the convex mix of bytes never leaves [0, 255]).
+constexpr int RZ2_T = 256, RZ2_R = 16, RZ2_NS = 2 * RZ2_T + 2;  // source columns per row (rx <= 2)
+
+__global__ void __launch_bounds__(RZ2_T)
+k_resize_rows(const uint8_t *__restrict__ src, int c, int h, int w, int64_t sp, int64_t scs, int64_t sfs,
+              int nh, int nw, double ry, double rx, uint8_t *__restrict__ dst, int64_t dp, int64_t dcs,
+              int64_t dfs) {
+    __shared__ double tab[256];
+    __shared__ double vrow[2][RZ2_NS];
+    __shared__ double rfy[RZ2_R], rgy[RZ2_R];
+    __shared__ int ry0[RZ2_R], ry1[RZ2_R];
+    const int tid = threadIdx.x;
+    tab[tid] = (double)tid;
+    const int jt0 = blockIdx.x * RZ2_T;
+    const int j = min(jt0 + tid, nw - 1);
+    auto col = [&](int jj, int &x0, int &x1, double &fx) {
+        double sx = __dsub_rn(__dmul_rn((double)jj + 0.5, rx), 0.5);
+        sx = fmin(fmax(sx, 0.0), (double)(w - 1));
+        x0 = (int)floor(sx);
+        x1 = min(x0 + 1, w - 1);
+        fx = __dsub_rn(sx, (double)x0);
+    };
+    int x0, x1, xa, xb, xe, xf;
+    double fx, fa, fe;
+    col(j, x0, x1, fx);
+    const double gx = __dsub_rn(1.0, fx);
+    col(jt0, xa, xb, fa);                      // first source column of the tile
+    col(min(jt0 + RZ2_T - 1, nw - 1), xe, xf, fe);  // last: x1 of the last column
+    const int xs0 = xa, ns = xf - xa + 1;
+    const int r0 = blockIdx.y * RZ2_R, nr = min(RZ2_R, nh - r0);
+    if (tid < nr) {
+        double sy = __dsub_rn(__dmul_rn((double)(r0 + tid) + 0.5, ry), 0.5);
+        sy = fmin(fmax(sy, 0.0), (double)(h - 1));
+        const int y0 = (int)floor(sy);
+        ry0[tid] = y0;
+        ry1[tid] = min(y0 + 1, h - 1);
+        rfy[tid] = __dsub_rn(sy, (double)y0);
+        rgy[tid] = __dsub_rn(1.0, rfy[tid]);
+    }
+    __syncthreads();
+    const int ch = blockIdx.z % c, f = blockIdx.z / c;
+    const uint8_t *p = src + (int64_t)f * sfs + (int64_t)ch * scs + xs0;
+    uint8_t *d = dst + (int64_t)f * dfs + (int64_t)ch * dcs + jt0 + tid;
+    const bool own = jt0 + tid < nw;
+    const int l0 = x0 - xs0, l1 = x1 - xs0;
+    for (int i = 0; i < nr; ++i) {
+        double *v = vrow[i & 1];
+        const uint8_t *p0 = p + (int64_t)ry0[i] * sp, *p1 = p + (int64_t)ry1[i] * sp;
+        const double fy = rfy[i], gy = rgy[i];
+        for (int k = tid; k < ns; k += RZ2_T)
+            v[k] = __dadd_rn(__dmul_rn(tab[__ldg(p0 + k)], gy), __dmul_rn(tab[__ldg(p1 + k)], fy));
+        __syncthreads();  // (two buffers: row i + 1 may overwrite the other one)
+        if (own) {
+            const double m = __dadd_rn(__dmul_rn(v[l0], gx), __dmul_rn(v[l1], fx));
+            d[(int64_t)(r0 + i) * dp] = (uint8_t)__double2loint(__dadd_rn(m, 6755399441055744.0));
+        }
+    }
+}
+
 // ---- launchers ------------------------------------------------------------
 
 void launch_bin_offset(const int8_t *bm, int64_t bp, int64_t bfs, int n, int h, int w, int b0,
@@ -436,6 +502,16 @@ void launch_scores_lattice(const int32_t *grid, const double *den, int n, int nc
 void launch_resize(const uint8_t *src, int n, int c, int h, int w, int64_t sp, int64_t scs,
                    int64_t sfs, int nh, int nw, double ry, double rx, uint8_t *dst, int64_t dp,
                    int64_t dcs, int64_t dfs, cudaStream_t st) {
+    static const int rows_path = [] {
+        const char *e = getenv("HOGB200_RESIZE_ROWS");  // 0: per-pixel kernel everywhere (A/B)
+        return e ? atoi(e) : 1;
+    }();
+    if (rows_path && rx <= 2.0) {
+        const dim3 grid((unsigned)((nw + RZ2_T - 1) / RZ2_T), (unsigned)((nh + RZ2_R - 1) / RZ2_R),
+                        (unsigned)(n * c));
+        k_resize_rows<<<grid, RZ2_T, 0, st>>>(src, c, h, w, sp, scs, sfs, nh, nw, ry, rx, dst, dp, dcs, dfs);
+        return;
+    }
     const dim3 grid((unsigned)blocks_for(nw, 128 * RZ_C), (unsigned)((nh + RZ_R - 1) / RZ_R),
                     (unsigned)(n * c));
     k_resize<<<grid, 128, 0, st>>>(src, c, h, w, sp, scs, sfs, nh, nw, ry, rx, dst, dp, dcs, dfs);

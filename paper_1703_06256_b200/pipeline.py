@@ -66,6 +66,45 @@ def default_chunks(n: int, pixels_per_frame: int) -> int:
     return max(1, min(n, int(env))) if env else 1
 
 
+def _i8_enabled() -> bool:
+    import os
+
+    return os.environ.get("HOGB200_SCORES_I8", "1") != "0"
+
+
+def i8_prepare(weights, cells_x: int, cells_y: int, bins: int):
+    """Host side of the exact integer score path (hog_scores_i8_prepare):
+    (fragment bytes, digits, scale) or None when the weights span more bits
+    than the integer path holds (HOG_ERANGE) or the geometry is outside it."""
+    import ctypes
+
+    lib = _native.load()
+    nbytes = lib.hog_scores_i8_frag_bytes(bins)
+    if nbytes == 0 or cells_x != 8 or not 1 <= cells_y <= 16:
+        return None
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    frag = np.zeros(nbytes, dtype=np.uint8)
+    digits, scale = ctypes.c_int(0), ctypes.c_double(0.0)
+    rc = lib.hog_scores_i8_prepare(w.ctypes.data, cells_x, cells_y, bins, frag.ctypes.data,
+                                   ctypes.byref(digits), ctypes.byref(scale))
+    if rc == _native.HOG_ERANGE:
+        return None
+    if rc != _native.HOG_OK:
+        raise _native.NativeError(f"hog_scores_i8_prepare failed ({rc}): "
+                                  f"{lib.hog_last_error().decode(errors='replace')}")
+    return frag, digits.value, scale.value
+
+
+def i8_weights(weights, cells_x: int, cells_y: int, bins: int, device):
+    """i8_prepare with the fragments uploaded: (device tensor, digits, scale) or None."""
+    r = i8_prepare(weights, cells_x, cells_y, bins)
+    if r is None:
+        return None
+    t = D.torch()
+    frag, digits, scale = r
+    return t.as_tensor(frag, device=device), digits, scale
+
+
 class HogPipeline:
     def __init__(self, n: int, channels: int, height: int, width: int, bins: int, *,
                  stride: int, cell: int = 8, window=(64, 128), normalization: str = "none",
@@ -140,6 +179,12 @@ class HogPipeline:
                 raise ValueError("weights length does not match the geometry")
             self.scores = t.empty((n, len(self.oys), len(self.oxs)), dtype=t.float64, device=dev)
             self.w_dev = t.as_tensor(self.weights, device=dev)
+        # exact integer-tensor-core scores (stride = cell, byte grid, 8 x <= 16
+        # cells, <= 20 bins, weights within 47 bits); else the fp64 kernels
+        self.i8 = None
+        if (self.weights is not None and self.fused and self.grid_u8 and g.cells_x == 8
+                and self.cell == self.stride and _i8_enabled()):
+            self.i8 = i8_weights(self.weights, g.cells_x, g.cells_y, bins, dev)
         if self.weights is not None or window_norm is not None:
             self.ri_dev = t.as_tensor(self.row_idx.astype(np.int32), device=dev)
             self.ci_dev = t.as_tensor(self.col_idx.astype(np.int32), device=dev)
@@ -408,7 +453,12 @@ class HogPipeline:
                          self.cell // self.stride if self.fused else 0, eps_term("l2"),
                          D.ptr(self.cell_sq) + 4 * a * self.ncy * (self.ncx + len(self.oxs)),
                          D.ptr(self.window_norms) + 8 * a * nwin, s)
-        if self.scores is not None and self.fused and g.cells_x == 8 and self.grid_u8:
+        if self.scores is not None and self.i8 is not None:
+            frag, digits, scale = self.i8
+            _native.call("hog_scores_lattice_i8", gp, n, self.ncy, self.ncx, self.bins,
+                         len(self.oys), len(self.oxs), g.cells_x, g.cells_y, D.ptr(frag), digits,
+                         scale, self.bias, sp, s)
+        elif self.scores is not None and self.fused and g.cells_x == 8 and self.grid_u8:
             _native.call("hog_scores_lattice_u8", gp, n, self.ncy, self.ncx,
                          self.bins, len(self.oys), len(self.oxs), g.cells_x, g.cells_y,
                          self.cell // self.stride, D.ptr(self.w_dev), self.bias, sp, s)
