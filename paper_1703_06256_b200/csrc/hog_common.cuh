@@ -114,6 +114,9 @@ constexpr int K2_G = 4;  // rows per phase-A/phase-B group
 #ifndef K2_RB_DECOUPLED
 #define K2_RB_DECOUPLED 0  // RB: 1 = producer/consumer named barriers instead of a CTA barrier per row (c2 -0.8 %, shard +1.2 %)
 #endif
+#ifndef K2_RB_P32
+#define K2_RB_P32 1  // RB: full 32-bit plane values in registers (k_planes FP)
+#endif
 #ifndef K2_FASTGROUP
 #define K2_FASTGROUP 1  // guard-free code path for full row groups (k_planes.cuh)
 #endif

@@ -192,6 +192,13 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
     // stored value (c2: 8 LDS.128 per row and lane, a short-scoreboard stall each)
     constexpr bool PREG = PR && NB * VC <= 32 && !TMA;
     uint32_t preg[PREG ? NB : 1][PREG ? VC : 1];
+    // FP (row-bulk variant): preg holds the lane's full 32-bit plane values P(Y, X),
+    // updated once per row by (row carry + strip-row prefix byte): one PRMT + one
+    // IADD3 per value and the staging store reads them in place, where the packed
+    // form costs a third instruction per value (unpack, 3-input add, u16x2 update).
+    // With per-thread global stores this lost (the next row's update waits on the
+    // store's source registers); staging stores release them at once.
+    constexpr bool FP = RB && PREG && VC == 4 && K2_RB_P32;
     constexpr int G = K2_G;
     const int nwarp = g.NWARP;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -428,6 +435,10 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                 for (int q = 0; q < 8; ++q)
                     if (q < warp) T += vtot[q * NB + n];
                 Lacc[n] = T;  // P(Y0, xs)
+                if constexpr (FP) {
+#pragma unroll
+                    for (int k = 0; k < VC; ++k) preg[FP ? n : 0][FP ? k : 0] += T;  // P(Y0, x + k + 1)
+                }
             }
         }
         if (warp == 0 && lane < NB) {  // P(Y0, .) at the next super-strip's left edge
@@ -491,7 +502,8 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                             uint32_t vals[VC];
 #pragma unroll
                             for (int k = 0; k < VC; ++k)
-                                vals[k] = preg[PREG ? n : 0][PREG ? k : 0] + Lacc[n] + half16(Q[n >> 1][k], n & 1);
+                                vals[k] = FP ? preg[PREG ? n : 0][PREG ? k : 0]
+                                             : preg[PREG ? n : 0][PREG ? k : 0] + Lacc[n] + half16(Q[n >> 1][k], n & 1);
 #pragma unroll
                             for (int k = 0; k < VC; k += 4)
                                 *reinterpret_cast<uint4 *>(sp + n * pns + k) =
@@ -590,7 +602,7 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
 #pragma unroll
             for (int n = 0; n < NB; ++n) {
                 const uint32_t pt_last = PREG ? preg[PREG ? n : 0][PREG ? VC - 1 : 0] : ptop[n * 32 * VC + VC - 1];
-                const uint32_t lv = pt_last + Lacc[n] + half16(Q[n >> 1][VC - 1], n & 1);
+                const uint32_t lv = FP ? pt_last : pt_last + Lacc[n] + half16(Q[n >> 1][VC - 1], n & 1);
                 const uint32_t r = __shfl_down_sync(FULL, lv, dR);
                 uint32_t l = __shfl_up_sync(FULL, lv, 1);
                 if (lane == 0) l = Lacc[n];
@@ -739,14 +751,33 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
             }
             // row i of the group: row carries (Lacc) and the strip sums Q
             auto row_update = [&](int i) {
+                        uint32_t Lrow[FP ? NB : 1];  // FP: the row's carry into the strip, per bin
 #pragma unroll
                         for (int w = 0; w < NW; ++w) {
                             const int e = i * NW + w;
                             const uint32_t L = __shfl_sync(FULL, Lsum[e / 32], e % 32);
                             Lacc[2 * w] += L & 0xffffu;
                             Lacc[2 * w + 1] += L >> 16;
+                            if constexpr (FP) {
+                                Lrow[FP ? 2 * w : 0] = L & 0xffffu;
+                                Lrow[FP ? 2 * w + 1 : 0] = L >> 16;
+                            }
                         }
-                        if constexpr (S8) {
+                        if constexpr (FP) {
+                            // P(Y+1, x+k+1) = P(Y, x+k+1) + Lrow + (strip-row prefix through column x+k)
+                            uint32_t r8[SW];
+#pragma unroll
+                            for (int j = 0; j < SW; ++j) r8[j] = ex[i][j];
+#pragma unroll
+                            for (int k = 0; k < VC; ++k) {
+                                const uint32_t s8 = bw[i].byte(k) << 3;
+#pragma unroll
+                                for (int j = 0; j < SW; ++j) r8[j] += shl_clamp(1u, s8 - 32u * j);
+#pragma unroll
+                                for (int n = 0; n < NB; ++n)
+                                    preg[FP ? n : 0][FP ? k : 0] += Lrow[FP ? n : 0] + byte_of(r8[n >> 2], n & 3);
+                            }
+                        } else if constexpr (S8) {
                             // strip-row prefix in u8x4 (<= 128 per bin), widened per column
                             uint32_t r8[SW];
 #pragma unroll

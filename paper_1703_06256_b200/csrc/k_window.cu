@@ -359,6 +359,7 @@ k_resize(const uint8_t *__restrict__ src, int c, int h, int w, int64_t sp, int64
     }
 }
 
+#if HOGB200_VARIANTS
 // Row-shared resize for downscales up to 2x (pyramid levels 1-3 of c5 hold
 // three quarters of the level pixels): per output row the CTA first forms the
 // vertical mix `rows` (detector.py:216) of every source column its 256 output
@@ -424,6 +425,8 @@ k_resize_rows(const uint8_t *__restrict__ src, int c, int h, int w, int64_t sp, 
         }
     }
 }
+
+#endif  // HOGB200_VARIANTS
 
 // ---- launchers ------------------------------------------------------------
 
@@ -502,16 +505,22 @@ void launch_scores_lattice(const int32_t *grid, const double *den, int n, int nc
 void launch_resize(const uint8_t *src, int n, int c, int h, int w, int64_t sp, int64_t scs,
                    int64_t sfs, int nh, int nw, double ry, double rx, uint8_t *dst, int64_t dp,
                    int64_t dcs, int64_t dfs, cudaStream_t st) {
+    // experiment builds only: the row-shared kernel measured slower on c5 (levels 1-3:
+    // 9.2 ms in 6 launches against ~4 ms for k_resize; profiles/r2/resize_rows_shared_ab.md)
     static const int rows_path = [] {
-        const char *e = getenv("HOGB200_RESIZE_ROWS");  // 0: per-pixel kernel everywhere (A/B)
-        return e ? atoi(e) : 1;
+        const char *e = HOGB200_VARIANTS ? getenv("HOGB200_RESIZE_ROWS") : nullptr;
+        return e ? atoi(e) : 0;
     }();
+#if HOGB200_VARIANTS
     if (rows_path && rx <= 2.0) {
         const dim3 grid((unsigned)((nw + RZ2_T - 1) / RZ2_T), (unsigned)((nh + RZ2_R - 1) / RZ2_R),
                         (unsigned)(n * c));
         k_resize_rows<<<grid, RZ2_T, 0, st>>>(src, c, h, w, sp, scs, sfs, nh, nw, ry, rx, dst, dp, dcs, dfs);
         return;
     }
+#else
+    (void)rows_path;
+#endif
     const dim3 grid((unsigned)blocks_for(nw, 128 * RZ_C), (unsigned)((nh + RZ_R - 1) / RZ_R),
                     (unsigned)(n * c));
     k_resize<<<grid, 128, 0, st>>>(src, c, h, w, sp, scs, sfs, nh, nw, ry, rx, dst, dp, dcs, dfs);

@@ -1,6 +1,6 @@
 """hog_resize_bilinear (detector.py:202-221) against the pinned oracle over
-downscale ratios on both sides of the row-shared kernel's limit (rx <= 2:
-k_resize_rows; above: the per-pixel k_resize), widths that leave partial
+downscale ratios on both sides of 2x (the limit of the experiment builds' row-shared
+k_resize_rows; the product library runs k_resize everywhere), widths that leave partial
 256-column tiles, RGB, and frame batches.  Bit-exact."""
 import numpy as np
 import pytest

@@ -9,7 +9,7 @@ mkdir -p build/var_$name
 objs=""
 # VARIANT_UNITS: units recompiled with the flags (default: the plane kernel + ABI)
 units=${VARIANT_UNITS:-"hog_abi k_planes_a k_planes_b k_planes_c k_planes_d k_window"}
-for u in hog_abi k_bin k_bin_oct k_planes_a k_planes_b k_planes_c k_planes_d k_window k_scores k_detect k_rect; do
+for u in hog_abi k_bin k_bin_oct k_planes_a k_planes_b k_planes_c k_planes_d k_window k_scores k_scores_i8 k_detect k_rect; do
   case " $units " in *" $u "*) ;; *) objs="$objs build/obj/$u.o";; esac
 done
 for u in $units; do
