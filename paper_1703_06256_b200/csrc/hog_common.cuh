@@ -105,6 +105,9 @@ struct GridOut {
 };
 
 constexpr int K2_G = 4;  // rows per phase-A/phase-B group
+#ifndef K2_GW
+#define K2_GW 2  // the same for NW >= 6 (<= K2_G: the shared layout is sized for K2_G); c5 61.6 -> 61.2 ms against 4
+#endif
 #ifndef K2_RB_ROWS
 #define K2_RB_ROWS 2  // RB: plane rows per staging slot (one bulk copy and one barrier per slot)
 #endif
@@ -115,7 +118,7 @@ constexpr int K2_G = 4;  // rows per phase-A/phase-B group
 #define K2_RB_DECOUPLED 0  // RB: 1 = producer/consumer named barriers instead of a CTA barrier per row (c2 -0.8 %, shard +1.2 %)
 #endif
 #ifndef K2_RB_P32
-#define K2_RB_P32 1  // RB: full 32-bit plane values in registers (k_planes FP)
+#define K2_RB_P32 0  // RB: 1 = full 32-bit plane values in registers (k_planes FP); measured 2 % slower on c2
 #endif
 #ifndef K2_FASTGROUP
 #define K2_FASTGROUP 1  // guard-free code path for full row groups (k_planes.cuh)
@@ -130,12 +133,31 @@ constexpr int K2_G = 4;  // rows per phase-A/phase-B group
 #ifndef K2_PTOP_REG
 #define K2_PTOP_REG 1
 #endif
+#ifndef K2_MINB
+#define K2_MINB 2
+#endif
+#ifndef K2_MAXT_WIDE
+#define K2_MAXT_WIDE 192  // CTA size bound of the wide variants (NW >= 6; experiment knob)
+#endif
+#ifndef K2_MINB_WIDE
+#define K2_MINB_WIDE K2_MINB
+#endif
+#ifndef K2_MAXT_MID
+#define K2_MAXT_MID 192  // the same for 9-10 bins at 4 columns per lane (c3)
+#endif
+#ifndef K2_MINB_MID
+#define K2_MINB_MID K2_MINB
+#endif
 // Plane-kernel CTA size bound.  preg: the small variants (<= 8 bins, 4 columns
 // per lane) keep the band's top row in 32 registers instead of shared memory,
 // bounded at 192 threads (170 registers at 2 CTAs/SM); chosen when a band's
 // strips fit 6 warps (make_geom), else the 256-thread variant runs.
 __host__ __device__ constexpr int k2_maxt(int nw, int vc, bool preg = false) {
-    return (vc == 8 || nw >= 5 || preg) ? 192 : 256;
+    return nw >= 6 ? K2_MAXT_WIDE : (nw == 5 && vc == 4) ? K2_MAXT_MID : (vc == 8 || nw >= 5 || preg) ? 192 : 256;
+}
+// resident CTAs per SM the register budget is set for (__launch_bounds__ second argument)
+__host__ __device__ constexpr int k2_minb(int nw, int vc) {
+    return nw >= 6 ? K2_MINB_WIDE : (nw == 5 && vc == 4) ? K2_MINB_MID : K2_MINB;
 }
 
 // Inputs of the fused plane kernel (binning inside k_planes, band carries by

@@ -166,9 +166,6 @@ __device__ __forceinline__ void bin_rows(const FusedIn &fi, const TileGeom &g, i
 //   Lacc(Y) = P(Y, xs)                  -- one value per bin, uniform over the warp
 //   Q(Y, X) = sum_{Y0 <= y < Y} count of row y in [xs, X)  -- <= (R+halo)*32*VC < 2^16,
 //             so two bins share one register (u16x2) and a row update is one add
-#ifndef K2_MINB
-#define K2_MINB 2
-#endif
 
 // CH > 0: fused variant -- the CTA bins its own rows from the frame (CH
 // channels) and gets the column counts above its band by decoupled look-back
@@ -182,7 +179,7 @@ __device__ __forceinline__ void bin_rows(const FusedIn &fi, const TileGeom &g, i
 // releases the slot on empty[slot] once the TMA engine has read it.  The
 // compute warps synchronise among themselves with named barrier 1.
 template <int NW, int KR, int VC, bool VEC, int CH = 0, bool TMA = false, bool PR = false, bool RB = false>
-__global__ void __launch_bounds__(k2_maxt(NW, VC, PR), K2_MINB)
+__global__ void __launch_bounds__(k2_maxt(NW, VC, PR), k2_minb(NW, VC))
 k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, GridOut go,
          TileGeom g, Scratch sc, FusedIn fi) {
     extern __shared__ __align__(16) uint32_t smem[];
@@ -196,10 +193,12 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
     // updated once per row by (row carry + strip-row prefix byte): one PRMT + one
     // IADD3 per value and the staging store reads them in place, where the packed
     // form costs a third instruction per value (unpack, 3-input add, u16x2 update).
-    // With per-thread global stores this lost (the next row's update waits on the
-    // store's source registers); staging stores release them at once.
+    // Measured slower with per-thread global stores and with staging stores alike
+    // (c2 1.015 against 0.995 ms: the row update then waits on the registers the
+    // row's STS.128 still read), so it is off (K2_RB_P32 = 0; experiment builds).
     constexpr bool FP = RB && PREG && VC == 4 && K2_RB_P32;
-    constexpr int G = K2_G;
+    // rows per phase-A/phase-B group (K2_GW: experiment knob for the wide variants, NW >= 6)
+    constexpr int G = NW >= 6 ? K2_GW : K2_G;
     const int nwarp = g.NWARP;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __shared__ int tk;
