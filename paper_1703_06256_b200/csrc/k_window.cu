@@ -344,9 +344,12 @@ k_resize(const uint8_t *__restrict__ src, int c, int h, int w, int64_t sp, int64
             const double a1 = (double)__ldg(p0 + x1[q]), b1 = (double)__ldg(p1 + x1[q]);
             const double r0 = __dadd_rn(__dmul_rn(a0, gy), __dmul_rn(b0, fy));
             const double rr1 = __dadd_rn(__dmul_rn(a1, gy), __dmul_rn(b1, fy));
-            double m = rint(__dadd_rn(__dmul_rn(r0, gx[q]), __dmul_rn(rr1, fx[q])));
-            m = fmin(fmax(m, 0.0), 255.0);
-            word |= (uint32_t)m << (8 * q);
+            // np.rint + clip (detector.py:219): the convex mix of bytes stays within
+            // [0, 255 + 1e-13], so rint alone lands in 0..255, and adding 1.5 * 2^52
+            // rounds to the nearest even integer like rint, leaving it in the low word
+            const double m = __dadd_rn(__dadd_rn(__dmul_rn(r0, gx[q]), __dmul_rn(rr1, fx[q])),
+                                       6755399441055744.0);
+            word |= ((uint32_t)__double2loint(m) & 0xffu) << (8 * q);
         }
         uint8_t *dr = d + (int64_t)r * dp;
         if (full) {
