@@ -120,6 +120,9 @@ constexpr int K2_G = 4;  // rows per phase-A/phase-B group
 #ifndef K2_RB_P32
 #define K2_RB_P32 0  // RB: 1 = full 32-bit plane values in registers (k_planes FP); measured 2 % slower on c2
 #endif
+#ifndef K2_PAIR256
+#define K2_PAIR256 0  // 256-bit plane stores by lane pairs (k_planes PAIR; experiment knob)
+#endif
 #ifndef K2_FASTGROUP
 #define K2_FASTGROUP 1  // guard-free code path for full row groups (k_planes.cuh)
 #endif

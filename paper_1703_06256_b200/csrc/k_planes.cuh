@@ -197,6 +197,9 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
     // (c2 1.015 against 0.995 ms: the row update then waits on the registers the
     // row's STS.128 still read), so it is off (K2_RB_P32 = 0; experiment builds).
     constexpr bool FP = RB && PREG && VC == 4 && K2_RB_P32;
+    // PAIR (experiment knob K2_PAIR256): 256-bit plane stores for the 4-columns-per-lane
+    // variants, the halves traded between lane pairs by shuffle
+    constexpr bool PAIR = K2_PAIR256 && VC == 4 && VEC && !TMA && !RB && CH == 0;
     // rows per phase-A/phase-B group (K2_GW: experiment knob for the wide variants, NW >= 6)
     constexpr int G = NW >= 6 ? K2_GW : K2_G;
     const int nwarp = g.NWARP;
@@ -559,6 +562,46 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
                                  : "memory");
                 else
                     *p0 = 0;
+            }
+            if constexpr (PAIR) {
+                // lane pairs trade halves so that each lane writes 8 adjacent columns of one
+                // bin with one 256-bit store: the even lane bin n, the odd lane bin n + 1
+                const bool oddl = (lane & 1) != 0;
+                const bool stp = oddl ? X0 - 4 <= g.w && active && own : st;  // the pair's even lane stores
+                int32_t *pe = prow - (oddl ? 4 : 0) + (oddl ? pns : 0);
+                auto value4 = [&](int n, uint32_t (&v)[4]) {
+                    if constexpr (PREG) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) v[k] = preg[PREG ? n : 0][PREG ? k : 0];
+                    } else {
+                        const uint4 t4 = *reinterpret_cast<const uint4 *>(ptop + n * 32 * VC);
+                        v[0] = t4.x, v[1] = t4.y, v[2] = t4.z, v[3] = t4.w;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) v[k] += Lacc[n] + half16(Q[n >> 1][k], n & 1);
+                };
+#pragma unroll
+                for (int n = 0; n < NB; n += 2) {
+                    uint32_t a[4], b[4];
+                    value4(n, a);
+                    if (n + 1 < NB - 1 || !odd) {
+                        value4(n + 1, b);
+                        uint32_t rcv[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) rcv[k] = __shfl_xor_sync(FULL, oddl ? a[k] : b[k], 1);
+                        if (stp)
+                            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(pe + n * pns),
+                                         "r"(oddl ? rcv[0] : a[0]), "r"(oddl ? rcv[1] : a[1]),
+                                         "r"(oddl ? rcv[2] : a[2]), "r"(oddl ? rcv[3] : a[3]),
+                                         "r"(oddl ? b[0] : rcv[0]), "r"(oddl ? b[1] : rcv[1]),
+                                         "r"(oddl ? b[2] : rcv[2]), "r"(oddl ? b[3] : rcv[3])
+                                         : "memory");
+                    } else if (st) {  // odd bin count: the last bin leaves as before
+                        *reinterpret_cast<int4 *>(prow + n * pns) = make_int4((int)a[0], (int)a[1], (int)a[2], (int)a[3]);
+                    }
+                }
+                prow += pp;
+                return;
             }
             if (st) {
                 int32_t *p = prow;
