@@ -120,6 +120,9 @@ constexpr int K2_G = 4;  // rows per phase-A/phase-B group
 #ifndef K2_RB_P32
 #define K2_RB_P32 0  // RB: 1 = full 32-bit plane values in registers (k_planes FP); measured 2 % slower on c2
 #endif
+#ifndef K2_STORE_HINT
+#define K2_STORE_HINT 0  // plane stores with an L2 evict-first hint (experiment knob)
+#endif
 #ifndef K2_PAIR256
 #define K2_PAIR256 0  // 256-bit plane stores by lane pairs (k_planes PAIR; experiment knob)
 #endif
@@ -249,9 +252,18 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *b, uint32_t parity) {
     }
 }
 __device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
+#if K2_STORE_HINT
+    // planes are written once and never re-read by the pipeline: first to leave L2
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+                 "r"(smem_addr(ssrc)), "r"(bytes), "l"(pol)
+                 : "memory");
+#else
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
                  "r"(smem_addr(ssrc)), "r"(bytes)
                  : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>

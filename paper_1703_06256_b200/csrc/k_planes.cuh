@@ -10,11 +10,21 @@ template <int VC>
 __device__ __forceinline__ void store_chunk(int32_t *p, const uint32_t (&v)[VC], bool vec, int valid) {
     if (vec) {
         if constexpr (VC == 8) {
+#if K2_STORE_HINT
+            asm volatile("st.global.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]),
+#else
             asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]),
+#endif
                          "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                          : "memory");
         } else {
+#if K2_STORE_HINT
+            asm volatile("st.global.cs.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                         "r"(v[3])
+                         : "memory");
+#else
             *reinterpret_cast<int4 *>(p) = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+#endif
         }
     } else {
 #pragma unroll
