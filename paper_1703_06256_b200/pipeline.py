@@ -625,6 +625,26 @@ class PyramidPipeline:
             streams = int(os.environ.get("HOGB200_PYR_STREAMS", "4"))
         self.streams = max(1, min(int(streams), len(self.levels)))
         self._side = [t.cuda.Stream(device=self.device) for _ in range(self.streams - 1)]
+        import os
+
+        # level -> stream (a level's chunks stay on one stream: its buffers are reused in
+        # order) and the order levels are issued in within a chunk
+        #   HOGB200_PYR_ASSIGN  rr: level i on stream i mod S; lpt: largest level first onto
+        #                       the stream with the least pixels so far
+        #   HOGB200_PYR_ORDER   asc: level 0 first; desc: smallest level first; asc-desc:
+        #                       descending in the last chunk only (the step ends on big kernels)
+        assign = os.environ.get("HOGB200_PYR_ASSIGN", "rr")
+        self.order_mode = os.environ.get("HOGB200_PYR_ORDER", "asc")
+        nl = len(self.levels)
+        if assign == "lpt":
+            load = [0] * self.streams
+            self.level_stream = [0] * nl
+            for i, (_, _, w, h) in enumerate(self.levels):  # levels come largest first
+                k = min(range(self.streams), key=lambda j: (load[j], j))
+                self.level_stream[i] = k
+                load[k] += w * h
+        else:
+            self.level_stream = [i % self.streams for i in range(nl)]
 
     @on_device
     def upload(self, frames: np.ndarray):
@@ -664,8 +684,13 @@ class PyramidPipeline:
             # a partial last chunk runs through the level pipelines' own buffers
             # (they process p.n frames: direct pointers would run past the batch)
             whole = m == self.chunk
-            for i, ((level, factor, w, h), p) in enumerate(zip(self.levels, self.pipes)):
-                st = sts[i % len(sts)]
+            last = a + self.chunk >= self.n
+            idx = list(range(len(self.levels)))
+            if self.order_mode == "desc" or (self.order_mode == "asc-desc" and last):
+                idx.reverse()
+            for i in idx:
+                (level, factor, w, h), p = self.levels[i], self.pipes[i]
+                st = sts[self.level_stream[i] % len(sts)]
                 dst = p.frames
                 with t.cuda.stream(st):
                     if level == 0 and not whole:
