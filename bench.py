@@ -70,10 +70,13 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--e2e-chunk", type=int, default=64, help="frames per H2D/compute/D2H chunk")
+    ap.add_argument("--e2e-chunk", type=int, default=0,
+                    help="frames per H2D/compute/D2H chunk (0: a quarter of the step's frames, so "
+                         "every chunk has its own buffer set; measured best, profiles/r2/e2e_chunking_ab.txt)")
     ap.add_argument("--e2e-slots", type=int, default=4, help="pipelines/streams in flight (e2e)")
-    ap.add_argument("--e2e-tail", type=int, default=4,
-                    help="e2e: split the last chunk in this many pieces (shorter drain)")
+    ap.add_argument("--e2e-tail", type=int, default=1,
+                    help="split the step's last chunk in this many pieces (1: no split; steps overlap, "
+                         "so a short last chunk buys nothing)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the timed steps (and the e2e step) eagerly, no CUDA graph")
     ap.add_argument("--e2e-overlap", type=int, default=1,
@@ -944,6 +947,8 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
 
     from paper_1703_06256_b200 import synth
 
+    if chunk <= 0:  # four chunks per step, each with its own buffer set (nslots = 4)
+        chunk = (nf + 3) // 4
     chunk = max(1, min(nf, chunk))
     # job schedule: full chunks, with the last chunk split in `tail` pieces so
     # the work left after the final H2D (its compute + D2H) is short
