@@ -957,7 +957,6 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
         last = sizes.pop()
         sizes += [last // tail] * (tail - 1) + [last - (last // tail) * (tail - 1)]
     weights, bias = synth.make_weights(cfg) if cfg.scored else (None, 0.0)
-    nslots = max(1, min(nslots, len(sizes)))
     h2d, comp, d2h = (torch.cuda.Stream(device=dev) for _ in range(3))
     pipes = {}  # (slot, size) -> pipeline
 
@@ -968,12 +967,18 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
                                             weights=weights, bias=bias, device=dev)
         return pipes[(si, sz)]
 
+    # buffer sets: chunk j of a step runs on set j % nslots; with fewer chunks than sets
+    # (c1: one frame, one chunk) consecutive steps rotate over nslots // chunks groups of
+    # sets, so step k+1's copy and compute still overlap step k's result leaving
+    nslots_arg = max(1, nslots)
+    nslots = max(1, min(nslots_arg, len(sizes)))
+    reps = max(1, nslots_arg // len(sizes)) if overlap else 1
     jobs, a = [], 0
     for j, sz in enumerate(sizes):
-        jobs.append((a, a + sz, pipe(j % nslots, sz)))
+        jobs.append((a, a + sz, [pipe(r * nslots + j % nslots, sz) for r in range(reps)]))
         a += sz
     host_in = torch.from_numpy(frames).pin_memory()
-    res = jobs[0][2].result()
+    res = jobs[0][2][0].result()
     gather = open_gather(job, res.shape[1:], res.dtype, rank, barrier)
     host_out = gather.local()  # this shard's slice of the node-wide result buffer
 
@@ -987,8 +992,9 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
         for st in (h2d, comp, d2h):
             st.wait_stream(cur)
         last = {}  # pipeline -> (computed, left) events of its latest chunk
-        for _ in range(nsteps):
-            for a, b, q in jobs:
+        for step in range(nsteps):
+            for a, b, qs in jobs:
+                q = qs[step % len(qs)]
                 prev = last.get(id(q))
                 if prev is not None:
                     h2d.wait_event(prev[0])  # frames buffer free
@@ -1054,7 +1060,7 @@ def run_e2e(p, H, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrier, ch
                        "cudaHostRegister): the batch's results in frame order on the host"),
             "bytes_per_gpu": "h2d/d2h bytes are this rank's shard",
             "result": "cell grid" if not cfg.scored else "window scores",
-            "chunk_frames": sizes, "buffer_sets": nslots,
+            "chunk_frames": sizes, "buffer_sets": nslots * reps,
             "streams": "1 H2D + 1 compute + 1 D2H (in-order copies)", "cuda_graph": bool(use_graph),
             "steps_overlap": bool(overlap),
             "matches_device_run": ok}
