@@ -613,6 +613,10 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "k_planes", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_src,
+                         # the kernel is ~97 % stores: also against the write-only ceiling
+                         # (cudaMemset of the same bytes, 7,349 GB/s: profiles/r1_tma_store_ab.md)
+                         "write_only_ceiling": {"peak": 7349.0, "frac": achieved / 7349.0,
+                                                "source": "builder-measured cudaMemset rate, round 1"},
                          "alg_bytes_per_launch": plane_bytes / nch, "launches_per_step": nch,
                          "alg_bytes_def": "bin map read (1 B/px) + int32 planes written "
                                           "(4*N_b*(H+1)*(W+1)) + cell grid written "
