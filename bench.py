@@ -857,15 +857,16 @@ def run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrie
     src = p.src.data
 
     done_prev = {}  # chunk start -> events after the previous step's levels of that chunk
+    out_prev = {}   # chunk start -> events after the previous step's score copies of that chunk
 
     def step():
         """One e2e step.  A chunk's H2D copy waits only until the previous
         step's levels of that chunk have read the source frames, so step k+1's
         first chunk crosses PCIe while step k's last chunk is computing."""
-        nonlocal done_prev
+        nonlocal done_prev, out_prev
         cur = torch.cuda.current_stream()
         cout.wait_stream(cur)
-        ready, done = {}, {}
+        ready, done, out = {}, {}, {}
         with torch.cuda.stream(cin):
             for a in range(0, nf, p.chunk):
                 m = min(p.chunk, nf - a)
@@ -878,6 +879,10 @@ def run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrie
 
         def chunk_ready(a, m, st):
             st.wait_event(ready[a])
+            # this step's scores of the chunk overwrite what the previous step is still
+            # copying out: wait for that chunk's copies only (not for the whole step's)
+            for ev in out_prev.get(a, []):
+                st.wait_event(ev)
 
         def level_done(level, a, m, st):
             ev = torch.cuda.Event()
@@ -886,10 +891,12 @@ def run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrie
             cout.wait_event(ev)
             with torch.cuda.stream(cout):
                 host_out[level][a:a + m].copy_(p.scores[level][a:a + m], non_blocking=True)
+                left = torch.cuda.Event()
+                left.record(cout)
+            out.setdefault(a, []).append(left)
 
         p.run(cur, chunk_ready=chunk_ready, level_done=level_done)
-        cur.wait_stream(cout)  # the next step's scores overwrite what this step copies out
-        done_prev = done
+        done_prev, out_prev = done, out
 
     cin.wait_stream(torch.cuda.current_stream())
     for _ in range(max(1, W)):
@@ -900,6 +907,7 @@ def run_e2e_pyramid(p, cfg, frames, nf, K, W, dev, world, max_over_ranks, barrie
     t0.record()
     for _ in range(K):
         step()
+    torch.cuda.current_stream().wait_stream(cout)  # the last step's score maps have left
     t1.record()
     torch.cuda.current_stream().wait_stream(cin)
     torch.cuda.synchronize()
