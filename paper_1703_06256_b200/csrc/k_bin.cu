@@ -10,6 +10,36 @@ namespace hogb200 {
 #endif
 constexpr int K1U = K1_UNROLL;  // rows of k_grad_bin's row loop unrolled together
 
+// Bit-sliced per-(sub-band, column) counts for >= 9 bins (NWB >= 3): a pixel's bin becomes
+// a one-hot word (bit n = [bin == n], one SHL), the rows of a column are summed by
+// carry-save adders into 8 bit planes (plane j bit n = bit j of the count of bin n; counts
+// <= R1 <= 240), and the planes are turned into the u8x4 words of Scratch::C by 8x8 bit
+// transposes once per sub-band.  ~7 instructions per pixel for 18 bins against 16 for the
+// packed-byte adds (count_cols: one shifted add per u8x4 word and pixel).  Measured
+// bit-exact and SLOWER (c3 binning 0.183 -> 0.235 ms, c5 +1.3 ms): 72 registers instead
+// of 56 cost two resident CTAs per SM, and this kernel waits on the table gathers, not on
+// issue slots.  Experiment knob, off.
+#ifndef K1_SLICED
+#define K1_SLICED 0
+#endif
+
+__device__ __forceinline__ void csa3(uint32_t &sum, uint32_t &carry, uint32_t a, uint32_t b, uint32_t c) {
+    sum = a ^ b ^ c;
+    carry = (a & b) | (c & (a ^ b));
+}
+
+// 8x8 bit transpose: out byte n bit j = in byte j bit n
+__device__ __forceinline__ uint64_t bit_tr8x8(uint64_t x) {
+    uint64_t t;
+    t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+    x = x ^ t ^ (t << 7);
+    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+    x = x ^ t ^ (t << 14);
+    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+    x = x ^ t ^ (t << 28);
+    return x;
+}
+
 // ---------------------------------------------------------------------------
 // K1: gradient + LUT binning (gradient.py:95-121), optionally counting bins
 // per (band, column) for k_scan_cols.  One warp = R rows x 128 columns of
@@ -90,10 +120,8 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
     int8_t *bout = bm + (int64_t)f * bfs + (int64_t)y0 * bp + x;
     const uint8_t *pd = rowp(y0 + 2);  // row y+2, clamped to the last row
 
-    // unrolled so the LUT gathers of consecutive rows overlap (the kernel waits
-    // on gather latency, not on issue)
-#pragma unroll K1U
-    for (int y = y0; y < y1; ++y) {
+    // one row: gradients, table gather, bin-map store, window rotation; returns the 4 bin bytes
+    auto row = [&](int y) -> uint32_t {
         // row y+2 in flight while row y is binned
         uint32_t r3[CH], e3[CH];
 #pragma unroll
@@ -133,17 +161,6 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
         }
         if (inx) *reinterpret_cast<uint32_t *>(bout) = bins4;
         bout += bp;
-        if (COUNTS) {
-#if K1_SMEM_COUNTS
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int slot = min((int)byte_of(bins4, k), nbin);  // NO_BIN -> spare slot
-                cnt[(slot * 4 + k) * 32] += 1;
-            }
-#else
-            count_cols<NWB>(bins4, cc);
-#endif
-        }
 #pragma unroll
         for (int ch = 0; ch < CH; ++ch) {
             r0[ch] = r1[ch];
@@ -152,8 +169,85 @@ k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs
             e1[ch] = e2[ch];
             e2[ch] = e3[ch];
         }
+        return bins4;
+    };
+    constexpr bool SL = COUNTS && K1_SLICED && !K1_SMEM_COUNTS && NWB >= 3;
+    uint32_t qp[SL ? 8 : 1][SL ? 4 : 1];  // bit planes of the column counts (qp[0..2] = ones, twos, fours)
+    if constexpr (SL) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) qp[j][k] = 0;
+        uint32_t t2a[4] = {0, 0, 0, 0}, t4a[4] = {0, 0, 0, 0};
+        // row pairs; rows past y1 add nothing and flush the pending carries (a multiple of 8 rows)
+        const int npairs = ((y1 - y0 + 7) >> 3) << 2;
+        int y = y0;
+#pragma unroll 1
+        for (int pr = 0; pr < npairs; ++pr, y += 2) {
+            const uint32_t ba = y < y1 ? row(y) : 0xffffffffu;
+            const uint32_t bb = y + 1 < y1 ? row(y + 1) : 0xffffffffu;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t oa = shl_clamp(1u, byte_of(ba, k)), ob = shl_clamp(1u, byte_of(bb, k));
+                uint32_t c2;
+                csa3(qp[0][k], c2, qp[0][k], oa, ob);
+                if ((pr & 1) == 0) {
+                    t2a[k] = c2;
+                } else {
+                    uint32_t c4;
+                    csa3(qp[SL ? 1 : 0][k], c4, qp[SL ? 1 : 0][k], t2a[k], c2);
+                    if ((pr & 2) == 0) {
+                        t4a[k] = c4;
+                    } else {
+                        uint32_t c;
+                        csa3(qp[SL ? 2 : 0][k], c, qp[SL ? 2 : 0][k], t4a[k], c4);
+#pragma unroll
+                        for (int j = 3; j < 8; ++j) {
+                            const uint32_t q = qp[SL ? j : 0][k];
+                            qp[SL ? j : 0][k] = q ^ c;
+                            c &= q;
+                        }
+                    }
+                }
+            }
+        }
+        // planes -> C[f][b][x+k][w] (u8x4 of bins 4w..4w+3): byte group g8 holds bins 8 g8..8 g8+7
+        uint32_t *cp = sc.C + (((int64_t)f * g.nb1 + b) * g.Wc + x) * NWB;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+            for (int g8 = 0; g8 < (NWB + 1) / 2; ++g8) {
+                const uint32_t sel = 0x40u + 0x11u * g8;  // result bytes 0, 1 = byte g8 of a, byte g8 of b
+                const uint32_t lo = __byte_perm(__byte_perm(qp[0][k], qp[SL ? 1 : 0][k], sel),
+                                                __byte_perm(qp[SL ? 2 : 0][k], qp[SL ? 3 : 0][k], sel), 0x5410);
+                const uint32_t hi = __byte_perm(__byte_perm(qp[SL ? 4 : 0][k], qp[SL ? 5 : 0][k], sel),
+                                                __byte_perm(qp[SL ? 6 : 0][k], qp[SL ? 7 : 0][k], sel), 0x5410);
+                const uint64_t t = bit_tr8x8(((uint64_t)hi << 32) | lo);
+                cp[k * NWB + 2 * g8] = (uint32_t)t;
+                if (2 * g8 + 1 < NWB) cp[k * NWB + 2 * g8 + 1] = (uint32_t)(t >> 32);
+            }
+        }
+    } else {
+        // unrolled so the LUT gathers of consecutive rows overlap (the kernel waits
+        // on gather latency, not on issue)
+#pragma unroll K1U
+        for (int y = y0; y < y1; ++y) {
+            const uint32_t bins4 = row(y);
+            (void)bins4;
+            if (COUNTS) {
+#if K1_SMEM_COUNTS
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int slot = min((int)byte_of(bins4, k), nbin);  // NO_BIN -> spare slot
+                    cnt[(slot * 4 + k) * 32] += 1;
+                }
+#else
+                count_cols<NWB>(bins4, cc);
+#endif
+            }
+        }
     }
-    if (COUNTS && !K1_SMEM_COUNTS) store_cols<NWB>(g, sc, f, b, x, cc);
+    if (COUNTS && !K1_SMEM_COUNTS && !SL) store_cols<NWB>(g, sc, f, b, x, cc);
     if (COUNTS && K1_SMEM_COUNTS) {
         // C[f][b][x+k][w]: bins 4w..4w+3 of column x+k as u8x4 (counts <= R <= 240)
         uint32_t *cp = sc.C + (((int64_t)f * g.nb1 + b) * g.Wc + x) * NWB;
