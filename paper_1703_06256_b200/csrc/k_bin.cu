@@ -47,8 +47,13 @@ __device__ __forceinline__ uint64_t bit_tr8x8(uint64_t x) {
 // three-row window down the band, two rows of loads in flight; left/right
 // neighbours come from the adjacent lanes by shuffle.
 
+// resident CTAs per SM the register budget is set for (experiment knob; 1 = the compiler's choice)
+#ifndef K1_MINB
+#define K1_MINB 1
+#endif
+
 template <int CH, int NWB, bool COUNTS>
-__global__ void __launch_bounds__(K_THREADS)
+__global__ void __launch_bounds__(K_THREADS, K1_MINB)
 k_grad_bin(const uint8_t *__restrict__ img, int64_t ip, int64_t ics, int64_t ifs,
            const uint8_t *__restrict__ lut, int8_t *__restrict__ bm, int64_t bp, int64_t bfs,
            TileGeom g, Scratch sc) {
