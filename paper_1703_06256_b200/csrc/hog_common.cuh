@@ -104,7 +104,13 @@ struct GridOut {
     int u8;
 };
 
-constexpr int K2_G = 4;  // rows per phase-A/phase-B group
+#ifndef K2_GN
+#define K2_GN 4
+#endif
+constexpr int K2_G = K2_GN;  // rows per phase-A/phase-B group (NW < 6; experiment knob K2_GN)
+#ifndef K2_G8
+#define K2_G8 2  // the same for 8 columns per lane (c4: 1.871 -> 1.857 ms against 4; c2's 4-column variant loses 3.8 % at 2)
+#endif
 #ifndef K2_GW
 #define K2_GW 2  // the same for NW >= 6 (<= K2_G: the shared layout is sized for K2_G); c5 61.6 -> 61.2 ms against 4
 #endif

@@ -210,8 +210,9 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
     // PAIR (experiment knob K2_PAIR256): 256-bit plane stores for the 4-columns-per-lane
     // variants, the halves traded between lane pairs by shuffle
     constexpr bool PAIR = K2_PAIR256 && VC == 4 && VEC && !TMA && !RB && CH == 0;
-    // rows per phase-A/phase-B group (K2_GW: experiment knob for the wide variants, NW >= 6)
-    constexpr int G = NW >= 6 ? K2_GW : K2_G;
+    // rows per phase-A/phase-B group: 4; 2 for the wide variants (NW >= 6, K2_GW) and for
+    // 8 columns per lane (K2_G8), where the group's live scan state is largest
+    constexpr int G = NW >= 6 ? K2_GW : VC == 8 ? K2_G8 : K2_G;
     const int nwarp = g.NWARP;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __shared__ int tk;
