@@ -212,7 +212,8 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
     constexpr bool PAIR = K2_PAIR256 && VC == 4 && VEC && !TMA && !RB && CH == 0;
     // rows per phase-A/phase-B group: 4; 2 for the wide variants (NW >= 6, K2_GW) and for
     // 8 columns per lane (K2_G8), where the group's live scan state is largest
-    constexpr int G = NW >= 6 ? K2_GW : VC == 8 ? K2_G8 : K2_G;
+    // (the experiment-only fused path, CH > 0, was written for 4-row groups)
+    constexpr int G = CH > 0 ? K2_G : NW >= 6 ? K2_GW : VC == 8 ? K2_G8 : K2_G;
     const int nwarp = g.NWARP;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __shared__ int tk;
