@@ -503,6 +503,7 @@ static int pipeline_impl(const uint8_t *img, int n, int c, int h, int w, int64_t
     g.hb = halo_bot ? 1 : 0;
     oct_subbands(g, c, g.S1);  // never more sub-bands than the scratch was sized for
     rowbulk_geom(g, po, kr);
+    if (want_fused) g.PREG = 0, g.RB = 0;  // the fused kernel keeps the band's top row in shared memory
     Scratch sc{};
     size_t need = carve(g, nullptr, nullptr);
     if (scratch == nullptr || sbytes < need)
