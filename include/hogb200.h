@@ -61,6 +61,12 @@ const char *hog_version(void);
 /* Text of the last error raised on the calling thread ("" if none). */
 const char *hog_last_error(void);
 
+/* Number of kernels the calling thread's last hog_pipeline / hog_pipeline_slab call
+ * launched (binning, carry scan, planes: the carry scan is folded into the plane
+ * kernel for shapes with few bands, integral.py:75-79), so callers can report
+ * launch counts they did not have to guess. */
+int hog_last_pipeline_launches(void);
+
 /* Octant binning (N_b in {4, 8}).  gradient.py:55-72: the reference's
  * table for these bin counts is folded by its quarter/half-turn symmetry into
  * sign tests of four linear forms evaluated in registers (no table gather).

@@ -21,6 +21,7 @@ _P, _I, _L, _D, _SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_do
 SIGNATURES = {
     "hog_version": (ctypes.c_char_p, []),
     "hog_last_error": (ctypes.c_char_p, []),
+    "hog_last_pipeline_launches": (_I, []),
     "hog_plane_pitch": (_L, [_I]),
     "hog_lut_proof": (_I, [_P, _I, _P, _P]),
     "hog_lut_forget": (None, [_P]),

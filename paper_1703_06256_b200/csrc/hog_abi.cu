@@ -113,6 +113,9 @@ bool lut_proven(const uint8_t *lut, int bins, cudaStream_t st) {
 // Thread-local: a caller sets it around its own launches.
 thread_local int g_band_rows = 0;
 
+// kernels the last hog_pipeline / hog_pipeline_slab call of this thread launched
+thread_local int g_last_launches = 0;
+
 // k_planes shared memory per CTA must allow two resident CTAs per SM
 constexpr int K2_SMEM_BUDGET = 113 * 1024;
 
@@ -384,6 +387,8 @@ const char *hog_version(void) { return "hogb200 1.2 sm_100a"; }
 
 const char *hog_last_error(void) { return g_err.c_str(); }
 
+int hog_last_pipeline_launches(void) { return hogb200::g_last_launches; }
+
 int hog_lut_proof(const uint8_t *lut, int bins, long long *mismatches, hog_stream_t stream) {
     g_err.clear();
     if (!lut || !mismatches) return fail(HOG_EINVAL, "null pointer");
@@ -504,6 +509,17 @@ static int pipeline_impl(const uint8_t *img, int n, int c, int h, int w, int64_t
     oct_subbands(g, c, g.S1);  // never more sub-bands than the scratch was sized for
     rowbulk_geom(g, po, kr);
     if (want_fused) g.PREG = 0, g.RB = 0;  // the fused kernel keeps the band's top row in shared memory
+    // Few sub-bands above any band (c1's single frame aside: c2, c4, the multi-GPU shards):
+    // k_planes sums the sub-band counts itself when that reads at most HOGB200_NOSCAN_PCT
+    // (default 5) percent of the plane bytes it writes; k_scan_cols and V are skipped.
+    // A pure function of the geometry, so a caller that runs the stages in separate calls
+    // gets the same answer in each (the scan stage is then a no-op); not in slab mode (the
+    // scan adds the carry of the slabs above).
+    {
+        const int pct = env_int("HOGB200_NOSCAN_PCT", 5);
+        g.NOSCAN = (!want_fused && !col_base && !halo_top && !halo_bot && pct > 0 &&
+                    (int64_t)g.nb1 * g.NWB * 100 <= (int64_t)pct * 2 * g.R * bins) ? 1 : 0;
+    }
     Scratch sc{};
     size_t need = carve(g, nullptr, nullptr);
     if (scratch == nullptr || sbytes < need)
@@ -532,6 +548,7 @@ static int pipeline_impl(const uint8_t *img, int n, int c, int h, int w, int64_t
     // step): binning is latency-bound and starves at the plane kernel's
     // occupancy, so the default is the three-kernel path.
     const bool fused = want_fused && g.nss == 1 && !halo_top && !halo_bot && !col_base;
+    g_last_launches = 0;
     if (fused) {
         FusedIn fi{img, ip, ics, ifs, lut, sc.flags, sc.flags + (size_t)g.n * g.nb2};
         cudaMemsetAsync(sc.flags, 0, sizeof(uint32_t) * ((size_t)g.n * g.nb2 + 1), st);
@@ -539,16 +556,24 @@ static int pipeline_impl(const uint8_t *img, int n, int c, int h, int w, int64_t
         mark(1);
         mark(2);
         launch_planes(g.NW, kr, c, bm, bp, bfs, po, go, g, sc, fi, st);
+        g_last_launches = 1;
         mark(3);
     } else {
         mark(0);
-        if (stages & HOG_STAGE_BIN)
+        if (stages & HOG_STAGE_BIN) {
             launch_grad_bin(g.NWB, c, true, img, ip, ics, ifs, lut, bm, bp, bfs, g, sc, st);
+            ++g_last_launches;
+        }
         mark(1);
-        if (stages & HOG_STAGE_SCAN) launch_scan(g.NW, g, sc, st);
+        if ((stages & HOG_STAGE_SCAN) && !g.NOSCAN) {
+            launch_scan(g.NW, g, sc, st);
+            ++g_last_launches;
+        }
         mark(2);
-        if (stages & HOG_STAGE_PLANES)
+        if (stages & HOG_STAGE_PLANES) {
             launch_planes(g.NW, kr, 0, bm, bp, bfs, po, go, g, sc, FusedIn{}, st);
+            ++g_last_launches;
+        }
         mark(3);
     }
     return check_launch("hog_pipeline");

@@ -60,6 +60,7 @@ struct TileGeom {
     int SEGW;   // TMA: staged columns per bin row = NWARP*Ws + 8 (32-B aligned front pad)
     int RB;     // whole plane rows staged in shared memory, one bulk copy per row (k_planes RB)
     int RBP;    // RB: words per bin row in the slot (= the plane pitch pns)
+    int NOSCAN; // k_planes sums the sub-band counts above its band itself (no k_scan_cols launch, no V)
 };
 
 // Scratch arrays (device), carved from the caller's scratch buffer.

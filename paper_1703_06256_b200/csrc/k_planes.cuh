@@ -401,6 +401,24 @@ k_planes(const int8_t *__restrict__ bm, int64_t bp, int64_t bfs, PlaneOut po, Gr
             __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) st_release_gpu(flags + b, 2u);
+        } else if (g.NOSCAN) {
+            // few sub-bands above any band: the CTA sums their u8x4 counts itself, which
+            // saves the carry-scan launch and the V round trip (integral.py:75-79: the
+            // column recurrence across bands)
+            if (active && b > 0 && x < g.Wc) {
+                const uint32_t *cq = sc.C + ((int64_t)f * g.nb1 * g.Wc + x) * NWB;
+                const int64_t cstep = (int64_t)g.Wc * NWB;
+                for (int q = b * g.S1; q > 0; --q, cq += cstep) {
+#pragma unroll
+                    for (int k = 0; k < VC; ++k)
+#pragma unroll
+                        for (int wb = 0; wb < NWB; ++wb) {
+                            const uint32_t c4 = __ldg(cq + k * NWB + wb);
+                            vreg[2 * wb][k] += widen_half(c4, 0);
+                            if (2 * wb + 1 < NW) vreg[2 * wb + 1 < NW ? 2 * wb + 1 : 0][k] += widen_half(c4, 1);
+                        }
+                }
+            }
         } else if (active && (b > 0 || sc.base) && x < g.Wc) {  // band 0: zero, or the slab carry
 #pragma unroll
             for (int w = 0; w < NW; ++w)

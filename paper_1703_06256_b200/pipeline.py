@@ -313,6 +313,9 @@ class HogPipeline:
                      if self.fused else None,
                      D.ptr(scr), sb, stages | (_native.STAGE_GRID_U8 if self.grid_u8 else 0), evs,
                      D.stream_handle(stream))
+        # kernels this call launched (the library folds the carry scan into the plane
+        # kernel for shapes with few bands)
+        self._core_launches = getattr(self, "_core_launches", 0) + _native.load().hog_last_pipeline_launches()
 
     @on_device
     def _grouped_call(self, base, a, b, fr, bm, pl, scr, sb, stages, evs, stream):
@@ -342,6 +345,14 @@ class HogPipeline:
         writes its slice of the pyramid's score maps directly)."""
         t = D.torch()
         main = stream if stream is not None else t.cuda.current_stream(self.device)
+        self._core_launches = 0
+        try:
+            return self._run(main, plane_events, frames_ptr, scores_ptr, pipelined)
+        finally:
+            self._core_run = self._core_launches
+
+    def _run(self, main, plane_events, frames_ptr, scores_ptr, pipelined):
+        t = D.torch()
         if pipelined and self.chunks == 1 and self.scores is not None:
             # consecutive batches overlap: this batch's binning + carry scan run
             # while the previous batch's scores are still computing (on
@@ -502,6 +513,8 @@ class HogPipeline:
 
     def launches_per_run(self) -> int:
         k = 3 * self.chunks  # grad_bin + carry scan + planes per chunk
+        if getattr(self, "_core_run", 0):  # counted by the library during the last run()
+            k = self._core_run
         if self.bins > MAX_PIPELINE_BINS:  # grad_bin + per bin group: offset, counts, scan, planes
             k = (1 + 4 * -(-self.bins // 16)) * self.chunks
         post = (0 if self.fused else 1) + (1 if self.denom is not None else 0) + \
