@@ -123,6 +123,10 @@ int hog_integral(const int8_t *binmap, int n, int h, int w, int64_t bm_pitch, in
  * then points to uint8 [n][ncy][ncx][bins] (exact: a cell count is <= cell*cell).  A caller may run the stages of one
  * frame batch as separate calls on different streams (stage order per batch,
  * same scratch), e.g. to bin batch j+1 while batch j writes its planes.
+ * For shapes with few bands per frame the carry scan (HOG_STAGE_SCAN: the column
+ * recurrence of integral.py:75-79 across bands) is folded into the plane kernel
+ * and that stage launches nothing; the choice depends only on the shape, so
+ * separate calls for one batch agree (hog_last_pipeline_launches() reports it).
  * stage_events: NULL, or 4 cudaEvent_t recorded on `stream` before the
  * binning kernel, before the carry scans, before the plane kernel and after
  * it (lets a caller time each stage inside a larger timed region). */
